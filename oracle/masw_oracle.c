@@ -1,0 +1,615 @@
+/*
+ * oracle/masw_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU fp64 reference for the MASW theoretical
+ * dispersion curve of Kump & Martin, "MASWAccelerated" (arXiv:2003.02256), written
+ * from the paper and the readings listed in DESIGN.md ("Readings").
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference arm
+ * may load this library.  It shares no code, header, table or constant generator
+ * with the CUDA product (paper_2003_02256_b200/csrc); neither side includes the other.
+ *
+ * What it computes, step by step:
+ *   O0 validate            oracle_validate()
+ *   O1 wavenumber          k = 2*pi/lambda                          (reading S2)
+ *   O2 velocity perturb    c' = c*(1-1e-4) while near a layer velocity (reading S4)
+ *   O3 layer element       Kausel-Roesset 4x4 element, complex arithmetic
+ *   O4 half-space element  2x2 element ("size 2(N+1)", S1, S22)
+ *   O5 determinant         DENSE complex LU with partial pivoting, det kept as
+ *                          (complex mantissa, binary exponent)
+ *   O6 sign                sgn(Re det)
+ *   O7 scan                Algorithm 1, lazily in ascending c, first change -> V[n]
+ *                                                                         (PAPER.md:50-71, S6-S9)
+ *   O8 misfit              Algorithm 2, index-order sum / l
+ *   O9 ensemble            O7+O8 per model, argmin ties -> lowest id
+ *   O10 det grid           every (lambda, c) det, no early exit
+ *
+ * Deliberately unlike the product: the product never forms K and eliminates 2x2 blocks
+ * in real arithmetic; this file scatters every element into a dense complex n x n matrix
+ * (n = 2(N+1)) and factors it with pivoting, O(n^3) per determinant, the way
+ * MASWaves does ("banded structure ... not utilized").
+ *
+ * Parity status per function: every function here is pinned by tests/test_oracle_pins.py
+ * (pins P1-P13, P15 of SURVEY.md §8(c)); see DESIGN.md "Oracle pins".
+ *
+ * Threads: rows (one (model, lambda) pair each) are independent ("no
+ * dependence on other wavelength values"), so oracle_curve/oracle_ensemble run rows on
+ * pthreads; each row's arithmetic is exactly the serial Algorithm 1.
+ */
+#include <complex.h>
+#include <math.h>
+#include <pthread.h>
+#include <stdatomic.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef double complex cplx;
+
+/* Status codes (same numeric meaning as documented in DESIGN.md; defined independently). */
+#define OR_OK 0
+#define OR_WARN_NO_SIGN_CHANGE 1
+#define OR_E_ARG (-1)
+#define OR_E_MODEL (-2)
+#define OR_E_GRID (-3)
+#define OR_E_RANGE (-4)
+#define OR_E_NONFINITE (-5)
+
+#define OR_IDX_NO_CHANGE (-1)
+#define OR_IDX_NONFINITE (-2)
+
+/* O1: 2*pi as the fp64 literal of reading S2/O1. */
+static const double OR_TWO_PI = 6.283185307179586;
+/* O0: overflow guard, reading S9: k*h must not exceed this. */
+static const double OR_MAX_KH = 350.0;
+/* O2: reading S4 (MASWaves rule). */
+static const double OR_PERTURB_TOL = 1e-4;
+static const double OR_PERTURB_FACTOR = 1e-4;
+
+/* ------------------------------------------------------------------ O0 validation */
+
+static int finite_all(const double *x, int64_t n)
+{
+    for (int64_t i = 0; i < n; ++i)
+        if (!isfinite(x[i])) return 0;
+    return 1;
+}
+
+/* Validate one model (SPEC.md:36 invariants: h>0, rho>0, beta>0, alpha>beta). */
+int oracle_validate_model(int32_t N, const double *h, const double *alpha,
+                          const double *beta, const double *rho)
+{
+    if (N < 1 || !h || !alpha || !beta || !rho) return OR_E_ARG;
+    if (!finite_all(h, N) || !finite_all(alpha, N + 1) || !finite_all(beta, N + 1) ||
+        !finite_all(rho, N + 1))
+        return OR_E_NONFINITE;
+    for (int e = 0; e < N; ++e)
+        if (!(h[e] > 0.0)) return OR_E_MODEL;
+    for (int e = 0; e <= N; ++e) {
+        if (!(rho[e] > 0.0) || !(beta[e] > 0.0) || !(alpha[e] > beta[e])) return OR_E_MODEL;
+    }
+    return OR_OK;
+}
+
+/* Validate the (lambda, c) grid: L>=1, lambda>0; V>=2, c strictly increasing, c0>0
+ * (reading S9), and the range guard k*h <= 350 (S9). */
+static int validate_grid(const double *lam, int64_t L, const double *c, int64_t V)
+{
+    if (!lam || !c || L < 1 || V < 2) return OR_E_ARG;
+    if (!finite_all(lam, L) || !finite_all(c, V)) return OR_E_NONFINITE;
+    for (int64_t i = 0; i < L; ++i)
+        if (!(lam[i] > 0.0)) return OR_E_GRID;
+    if (!(c[0] > 0.0)) return OR_E_GRID;
+    for (int64_t j = 1; j < V; ++j)
+        if (!(c[j] > c[j - 1])) return OR_E_GRID;
+    return OR_OK;
+}
+
+static int validate_range(int32_t N, const double *h, const double *lam, int64_t L)
+{
+    for (int64_t i = 0; i < L; ++i) {
+        double k = OR_TWO_PI / lam[i];
+        for (int e = 0; e < N; ++e)
+            if (k * h[e] > OR_MAX_KH) return OR_E_RANGE;
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ O1, O2 */
+
+double oracle_wavenumber(double lambda) { return OR_TWO_PI / lambda; }
+
+/* O2 (reading S4): while c' lies within 1e-4 m/s of any alpha_e or beta_e (e = 0..N,
+ * half-space included), c' <- c' * (1 - 1e-4).  The reported C_t stays the grid value. */
+double oracle_perturb_velocity(int32_t N, const double *alpha, const double *beta, double c)
+{
+    for (;;) {
+        int near = 0;
+        for (int e = 0; e <= N; ++e) {
+            if (fabs(c - alpha[e]) < OR_PERTURB_TOL || fabs(c - beta[e]) < OR_PERTURB_TOL) {
+                near = 1;
+                break;
+            }
+        }
+        if (!near) return c;
+        c = c * (1.0 - OR_PERTURB_FACTOR);
+    }
+}
+
+/* ------------------------------------------------------------------ O3 layer element
+ * Kausel-Roesset / MASWaves layer stiffness (the paper cites the
+ * method only, "stiffness matrix method (Kausel, 1981)"; reading S1).
+ * Complex arithmetic throughout, principal square roots (reading S3):
+ *   r = sqrt(1 - c^2/alpha^2), s = sqrt(1 - c^2/beta^2)
+ *   Cr = cosh(k r h), Sr = sinh(k r h), Cs = cosh(k s h), Ss = sinh(k s h)
+ *   D  = 2(1 - Cr Cs) + (1/(r s) + r s) Sr Ss,   f = k rho c^2 / D
+ *   k11 = f (Cr Ss/s - r Sr Cs)          k12 = f (Cr Cs - r s Sr Ss - 1) - k rho beta^2 (1 + s^2)
+ *   k13 = f (r Sr - Ss/s)                k14 = f (Cs - Cr)
+ *   k22 = f (Sr Cs/r - s Cr Ss)          k24 = f (s Ss - Sr/r)
+ *   Ke = [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12], [k14, k24, -k12, k22]]
+ * Local DOFs (u_top, w_top, u_bot, w_bot).
+ */
+static void layer_element(double h, double alpha, double beta, double rho, double k, double c,
+                          cplx Ke[4][4])
+{
+    cplx r = csqrt(1.0 - (c * c) / (alpha * alpha));
+    cplx s = csqrt(1.0 - (c * c) / (beta * beta));
+    cplx Cr = ccosh(k * r * h), Sr = csinh(k * r * h);
+    cplx Cs = ccosh(k * s * h), Ss = csinh(k * s * h);
+    cplx D = 2.0 * (1.0 - Cr * Cs) + (1.0 / (r * s) + r * s) * Sr * Ss;
+    cplx f = k * rho * c * c / D;
+    cplx k11 = f * (Cr * Ss / s - r * Sr * Cs);
+    cplx k12 = f * (Cr * Cs - r * s * Sr * Ss - 1.0) - k * rho * beta * beta * (1.0 + s * s);
+    cplx k13 = f * (r * Sr - Ss / s);
+    cplx k14 = f * (Cs - Cr);
+    cplx k22 = f * (Sr * Cs / r - s * Cr * Ss);
+    cplx k24 = f * (s * Ss - Sr / r);
+    cplx M[4][4] = {{k11, k12, k13, k14},
+                    {k12, k22, -k14, k24},
+                    {k13, -k14, k11, -k12},
+                    {k14, k24, -k12, k22}};
+    memcpy(Ke, M, sizeof(M));
+}
+
+/* Exported for the pins: Ke as 16 complex numbers, row-major, (re, im) interleaved. */
+void oracle_layer_element(double h, double alpha, double beta, double rho, double k, double c,
+                          double *out32)
+{
+    cplx Ke[4][4];
+    layer_element(h, alpha, beta, rho, k, c, Ke);
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            out32[2 * (4 * a + b)] = creal(Ke[a][b]);
+            out32[2 * (4 * a + b) + 1] = cimag(Ke[a][b]);
+        }
+}
+
+/* ------------------------------------------------------------------ O4 half-space element
+ *   K_hs = k rho beta^2 [[ r(1-s^2)/(1-rs),    (1-s^2)/(1-rs) - 2 ],
+ *                        [ (1-s^2)/(1-rs) - 2, s(1-s^2)/(1-rs)    ]]
+ * (reading S1, S22.)
+ */
+static void halfspace_element(double alpha, double beta, double rho, double k, double c,
+                              cplx Kh[2][2])
+{
+    cplx r = csqrt(1.0 - (c * c) / (alpha * alpha));
+    cplx s = csqrt(1.0 - (c * c) / (beta * beta));
+    double mu = k * rho * beta * beta;
+    cplx q = (1.0 - s * s) / (1.0 - r * s);
+    Kh[0][0] = mu * r * q;
+    Kh[0][1] = mu * q - 2.0 * mu;
+    Kh[1][0] = Kh[0][1];
+    Kh[1][1] = mu * s * q;
+}
+
+void oracle_halfspace_element(double alpha, double beta, double rho, double k, double c,
+                              double *out8)
+{
+    cplx Kh[2][2];
+    halfspace_element(alpha, beta, rho, k, c, Kh);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            out8[2 * (2 * a + b)] = creal(Kh[a][b]);
+            out8[2 * (2 * a + b) + 1] = cimag(Kh[a][b]);
+        }
+}
+
+/* Dense global assembly: layer e adds Ke into rows/cols 2e..2e+3, the half-space adds
+ * K_hs into rows/cols 2N, 2N+1 (PAPER.md:78 order 2(N+1)).  c is used as
+ * given (callers pass the perturbed c'). */
+static void assemble(int32_t N, const double *h, const double *alpha, const double *beta,
+                     const double *rho, double k, double c, cplx *K /* [n*n] */)
+{
+    int n = 2 * (N + 1);
+    for (int i = 0; i < n * n; ++i) K[i] = 0.0;
+    for (int e = 0; e < N; ++e) {
+        cplx Ke[4][4];
+        layer_element(h[e], alpha[e], beta[e], rho[e], k, c, Ke);
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) K[(2 * e + a) * n + (2 * e + b)] += Ke[a][b];
+    }
+    cplx Kh[2][2];
+    halfspace_element(alpha[N], beta[N], rho[N], k, c, Kh);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) K[(2 * N + a) * n + (2 * N + b)] += Kh[a][b];
+}
+
+void oracle_assemble(int32_t N, const double *h, const double *alpha, const double *beta,
+                     const double *rho, double k, double c, double *out /* [n*n*2] */)
+{
+    int n = 2 * (N + 1);
+    cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    assemble(N, h, alpha, beta, rho, k, c, K);
+    for (int i = 0; i < n * n; ++i) {
+        out[2 * i] = creal(K[i]);
+        out[2 * i + 1] = cimag(K[i]);
+    }
+    free(K);
+}
+
+/* ------------------------------------------------------------------ O5 determinant
+ * Dense LU with partial pivoting (row of largest |a_ik|).  det = (-1)^swaps * prod u_kk,
+ * accumulated as mant * 2^exp2 with max(|Re mant|, |Im mant|) in [0.5, 1) (reading S14).
+ * Returns OR_OK, or OR_E_NONFINITE if any entry or pivot is not finite.  An all-zero
+ * pivot column gives det = 0 exactly (mant = 0, exp2 = 0).
+ */
+static int det_lu(int n, cplx *A, cplx *mant, int *exp2)
+{
+    for (int i = 0; i < n * n; ++i)
+        if (!isfinite(creal(A[i])) || !isfinite(cimag(A[i]))) return OR_E_NONFINITE;
+    cplx m = 1.0;
+    int ex = 0;
+    for (int kk = 0; kk < n; ++kk) {
+        int p = kk;
+        double best = cabs(A[kk * n + kk]);
+        for (int i = kk + 1; i < n; ++i) {
+            double v = cabs(A[i * n + kk]);
+            if (v > best) {
+                best = v;
+                p = i;
+            }
+        }
+        if (best == 0.0) {
+            *mant = 0.0;
+            *exp2 = 0;
+            return OR_OK;
+        }
+        if (p != kk) {
+            for (int j = 0; j < n; ++j) {
+                cplx t = A[kk * n + j];
+                A[kk * n + j] = A[p * n + j];
+                A[p * n + j] = t;
+            }
+            m = -m;
+        }
+        cplx piv = A[kk * n + kk];
+        for (int i = kk + 1; i < n; ++i) {
+            cplx l = A[i * n + kk] / piv;
+            for (int j = kk; j < n; ++j) A[i * n + j] -= l * A[kk * n + j];
+        }
+        m *= piv;
+        double t = fmax(fabs(creal(m)), fabs(cimag(m)));
+        if (!isfinite(t)) return OR_E_NONFINITE;
+        if (t == 0.0) {
+            *mant = 0.0;
+            *exp2 = 0;
+            return OR_OK;
+        }
+        int e2;
+        frexp(t, &e2);
+        m = ldexp(creal(m), -e2) + I * ldexp(cimag(m), -e2);
+        ex += e2;
+    }
+    *mant = m;
+    *exp2 = ex;
+    return OR_OK;
+}
+
+/* Exported for the pins: determinant of a dense complex matrix ((re, im) interleaved). */
+int oracle_det_dense(int32_t n, const double *a /* [n*n*2] */, double *mant2, int32_t *exp2)
+{
+    cplx *A = (cplx *)malloc(sizeof(cplx) * n * n);
+    for (int i = 0; i < n * n; ++i) A[i] = a[2 * i] + I * a[2 * i + 1];
+    cplx m = 0.0;
+    int e = 0;
+    int st = det_lu(n, A, &m, &e);
+    free(A);
+    mant2[0] = creal(m);
+    mant2[1] = cimag(m);
+    *exp2 = e;
+    return st;
+}
+
+/* O1-O5 for one (model, lambda, c): k, perturb, assemble, dense det. */
+static int det_at(int32_t N, const double *h, const double *alpha, const double *beta,
+                  const double *rho, double lambda, double c, cplx *K, cplx *mant, int *exp2)
+{
+    double k = OR_TWO_PI / lambda;
+    double cp = oracle_perturb_velocity(N, alpha, beta, c);
+    assemble(N, h, alpha, beta, rho, k, cp, K);
+    return det_lu(2 * (N + 1), K, mant, exp2);
+}
+
+int oracle_det(int32_t N, const double *h, const double *alpha, const double *beta,
+               const double *rho, double lambda, double c, double *mant2, int32_t *exp2)
+{
+    int n = 2 * (N + 1);
+    cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    cplx m = 0.0;
+    int e = 0;
+    int st = det_at(N, h, alpha, beta, rho, lambda, c, K, &m, &e);
+    free(K);
+    mant2[0] = creal(m);
+    mant2[1] = cimag(m);
+    *exp2 = e;
+    return st;
+}
+
+/* ------------------------------------------------------------------ O6 sign */
+static int sign_re(cplx m)
+{
+    double re = creal(m);
+    return (re > 0.0) - (re < 0.0);
+}
+
+/* ------------------------------------------------------------------ O7 scan (Algorithm 1)
+ * d_old = det(V[0]); d_new = det(V[1]); n = 1;
+ *   while sign(d_old) == sign(d_new): n++, d_old = d_new, d_new = det(V[n]);  C_t = V[n].
+ * Readings: 0 is a sign of its own (S6); returned velocity is the unperturbed V[n] (S7);
+ * no change over the grid -> idx -1, C_t NaN (S8); a non-finite det -> idx -2 (S9).
+ * *ndet counts the determinants evaluated.
+ */
+static void scan_row(int32_t N, const double *h, const double *alpha, const double *beta,
+                     const double *rho, double lambda, const double *c, int64_t V, cplx *K,
+                     double *ct, int32_t *idx, int64_t *ndet)
+{
+    int64_t count = 0;
+    int s_old = 0;
+    for (int64_t j = 0; j < V; ++j) {
+        cplx m = 0.0;
+        int e;
+        int st = det_at(N, h, alpha, beta, rho, lambda, c[j], K, &m, &e);
+        ++count;
+        if (st != OR_OK) {
+            *idx = OR_IDX_NONFINITE;
+            *ct = NAN;
+            *ndet = count;
+            return;
+        }
+        int s_new = sign_re(m);
+        if (j > 0 && s_new != s_old) {
+            *idx = (int32_t)j;
+            *ct = c[j];
+            *ndet = count;
+            return;
+        }
+        s_old = s_new;
+    }
+    *idx = OR_IDX_NO_CHANGE;
+    *ct = NAN;
+    *ndet = count;
+}
+
+/* ------------------------------------------------------------------ row threads */
+typedef struct {
+    int64_t M, L, V;
+    int32_t N;
+    const double *h, *alpha, *beta, *rho; /* SoA [M][N], [M][N+1] */
+    const double *lam, *c;
+    double *ct;     /* [M][L] */
+    int32_t *idx;   /* [M][L] */
+    int64_t *ndet;  /* [M][L] or NULL */
+    atomic_llong next;
+} rows_job;
+
+static void *rows_worker(void *arg)
+{
+    rows_job *J = (rows_job *)arg;
+    int n = 2 * (J->N + 1);
+    cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    const int64_t total = J->M * J->L;
+    for (;;) {
+        int64_t r = atomic_fetch_add(&J->next, 1);
+        if (r >= total) break;
+        int64_t m = r / J->L, i = r % J->L;
+        int32_t N = J->N;
+        int64_t nd = 0;
+        scan_row(N, J->h + m * N, J->alpha + m * (N + 1), J->beta + m * (N + 1),
+                 J->rho + m * (N + 1), J->lam[i], J->c, J->V, K, &J->ct[r], &J->idx[r], &nd);
+        if (J->ndet) J->ndet[r] = nd;
+    }
+    free(K);
+    return NULL;
+}
+
+static void run_rows(rows_job *J, int nthreads)
+{
+    atomic_init(&J->next, 0);
+    if (nthreads <= 1) {
+        rows_worker(J);
+        return;
+    }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * nthreads);
+    int started = 0;
+    for (int t = 0; t < nthreads; ++t)
+        if (pthread_create(&th[t], NULL, rows_worker, J) == 0) ++started;
+    if (started == 0) rows_worker(J);
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+    free(th);
+}
+
+/* ------------------------------------------------------------------ O8 misfit (Algorithm 2)
+ * e = 0; for i = 1..l: e += |C_t[i] - C_e[i]| / C_e[i];  m = e / l.
+ * Readings: e starts at 0, index order (S12); any non-finite C_t -> +inf (S8).
+ * Errors: l < 1 -> OR_E_ARG; C_e not finite -> OR_E_NONFINITE; C_e <= 0 -> OR_E_ARG.
+ */
+int oracle_misfit(const double *ct, const double *ce, int64_t L, double *out)
+{
+    if (!ct || !ce || !out || L < 1) return OR_E_ARG;
+    if (!finite_all(ce, L)) return OR_E_NONFINITE;
+    for (int64_t i = 0; i < L; ++i)
+        if (!(ce[i] > 0.0)) return OR_E_ARG;
+    double e = 0.0;
+    for (int64_t i = 0; i < L; ++i) {
+        if (!isfinite(ct[i])) {
+            *out = INFINITY;
+            return OR_OK;
+        }
+        e = e + fabs(ct[i] - ce[i]) / ce[i];
+    }
+    *out = e / (double)L;
+    return OR_OK;
+}
+
+/* Same sum in long double, for tolerance audits. */
+int oracle_misfit_ld(const double *ct, const double *ce, int64_t L, double *out)
+{
+    if (!ct || !ce || !out || L < 1) return OR_E_ARG;
+    long double e = 0.0L;
+    for (int64_t i = 0; i < L; ++i) {
+        if (!isfinite(ct[i])) {
+            *out = INFINITY;
+            return OR_OK;
+        }
+        e += fabsl((long double)ct[i] - (long double)ce[i]) / (long double)ce[i];
+    }
+    *out = (double)(e / (long double)L);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------ public: one curve */
+static int validate_all(int64_t M, int32_t N, const double *h, const double *alpha,
+                        const double *beta, const double *rho, const double *lam, int64_t L,
+                        const double *c, int64_t V)
+{
+    if (M < 0 || N < 1) return OR_E_ARG;
+    int st = validate_grid(lam, L, c, V);
+    if (st != OR_OK) return st;
+    for (int64_t m = 0; m < M; ++m) {
+        st = oracle_validate_model(N, h + m * N, alpha + m * (N + 1), beta + m * (N + 1),
+                                   rho + m * (N + 1));
+        if (st != OR_OK) return st;
+    }
+    for (int64_t m = 0; m < M; ++m) {
+        st = validate_range(N, h + m * N, lam, L);
+        if (st != OR_OK) return st;
+    }
+    return OR_OK;
+}
+
+static int worst_row_status(const int32_t *idx, int64_t n)
+{
+    for (int64_t r = 0; r < n; ++r)
+        if (idx[r] < 0) return OR_WARN_NO_SIGN_CHANGE;
+    return OR_OK;
+}
+
+/* C_t for one model (Algorithm 1 per wavelength).  ndet may be NULL. */
+int oracle_curve(int32_t N, const double *h, const double *alpha, const double *beta,
+                 const double *rho, const double *lam, int64_t L, const double *c, int64_t V,
+                 double *ct, int32_t *idx, int64_t *ndet, int32_t nthreads)
+{
+    int st = validate_all(1, N, h, alpha, beta, rho, lam, L, c, V);
+    if (st != OR_OK) return st;
+    rows_job J;
+    J.M = 1; J.L = L; J.V = V; J.N = N;
+    J.h = h; J.alpha = alpha; J.beta = beta; J.rho = rho;
+    J.lam = lam; J.c = c; J.ct = ct; J.idx = idx; J.ndet = ndet;
+    run_rows(&J, nthreads);
+    return worst_row_status(idx, L);
+}
+
+/* ------------------------------------------------------------------ O9 ensemble */
+int oracle_ensemble(int64_t M, int32_t N, const double *h, const double *alpha,
+                    const double *beta, const double *rho, const double *lam, int64_t L,
+                    const double *c, int64_t V, const double *ce, double *ct, int32_t *idx,
+                    double *misfit, int64_t *ndet, int64_t *best, int32_t nthreads)
+{
+    int st = validate_all(M, N, h, alpha, beta, rho, lam, L, c, V);
+    if (st != OR_OK) return st;
+    if (ce) {
+        if (!finite_all(ce, L)) return OR_E_NONFINITE;
+        for (int64_t i = 0; i < L; ++i)
+            if (!(ce[i] > 0.0)) return OR_E_ARG;
+    }
+    if (M == 0) {
+        if (best) *best = -1;
+        return OR_OK;
+    }
+    rows_job J;
+    J.M = M; J.L = L; J.V = V; J.N = N;
+    J.h = h; J.alpha = alpha; J.beta = beta; J.rho = rho;
+    J.lam = lam; J.c = c; J.ct = ct; J.idx = idx; J.ndet = ndet;
+    run_rows(&J, nthreads);
+    if (ce && misfit) {
+        for (int64_t m = 0; m < M; ++m) oracle_misfit(ct + m * L, ce, L, &misfit[m]);
+        if (best) {
+            int64_t b = 0;
+            for (int64_t m = 1; m < M; ++m)
+                if (misfit[m] < misfit[b]) b = m; /* strict: ties -> lowest id */
+            *best = b;
+        }
+    }
+    return worst_row_status(idx, M * L);
+}
+
+/* ------------------------------------------------------------------ O10 det grid
+ * Every (lambda_i, c_j) determinant, no early exit ("grid" view).
+ * Outputs [L][V]: mantissa (re, im) and exponent; status[L][V] (0 or OR_E_NONFINITE).
+ */
+typedef struct {
+    int32_t N;
+    const double *h, *alpha, *beta, *rho, *lam, *c;
+    int64_t L, V;
+    double *mre, *mim;
+    int32_t *ex, *status;
+    atomic_llong next;
+} grid_job;
+
+static void *grid_worker(void *arg)
+{
+    grid_job *G = (grid_job *)arg;
+    int n = 2 * (G->N + 1);
+    cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    for (;;) {
+        int64_t i = atomic_fetch_add(&G->next, 1);
+        if (i >= G->L) break;
+        for (int64_t j = 0; j < G->V; ++j) {
+            cplx m = 0.0;
+            int e = 0;
+            int st = det_at(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], K, &m, &e);
+            int64_t o = i * G->V + j;
+            G->mre[o] = creal(m);
+            G->mim[o] = cimag(m);
+            G->ex[o] = e;
+            if (G->status) G->status[o] = st;
+        }
+    }
+    free(K);
+    return NULL;
+}
+
+int oracle_det_grid(int32_t N, const double *h, const double *alpha, const double *beta,
+                    const double *rho, const double *lam, int64_t L, const double *c, int64_t V,
+                    double *mant_re, double *mant_im, int32_t *exp2, int32_t *status,
+                    int32_t nthreads)
+{
+    int st = validate_all(1, N, h, alpha, beta, rho, lam, L, c, V);
+    if (st != OR_OK) return st;
+    grid_job G;
+    G.N = N; G.h = h; G.alpha = alpha; G.beta = beta; G.rho = rho;
+    G.lam = lam; G.c = c; G.L = L; G.V = V;
+    G.mre = mant_re; G.mim = mant_im; G.ex = exp2; G.status = status;
+    atomic_init(&G.next, 0);
+    if (nthreads <= 1) {
+        grid_worker(&G);
+        return OR_OK;
+    }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * nthreads);
+    int started = 0;
+    for (int t = 0; t < nthreads; ++t)
+        if (pthread_create(&th[t], NULL, grid_worker, &G) == 0) ++started;
+    if (started == 0) grid_worker(&G);
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+    free(th);
+    return OR_OK;
+}
