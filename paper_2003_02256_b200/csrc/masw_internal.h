@@ -1,0 +1,66 @@
+// masw_internal.h -- declarations shared by the kernels TU and the C-ABI TU of libmasw.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace masw {
+
+// Device workspace of one call (allocated stream-ordered, zeroed before use).
+struct Workspace {
+    unsigned long long queue;          // next row to scan (work-stealing counter)
+    unsigned long long alg_dets;       // sum over rows of (event index + 1)
+    unsigned long long eval_dets;      // determinants evaluated incl. speculation
+    unsigned long long model_err;      // ~key of first bad model: key = m << 2 | class
+    unsigned long long h_max_bits;     // max h over all layers/models (positive doubles)
+    unsigned long long lam_min_nbits;  // ~bits(min lambda)
+    unsigned int grid_err;             // bit0 lambda nonfinite, bit1 c nonfinite, bit2 lambda<=0,
+                                       // bit3 c0<=0, bit4 c not increasing,
+                                       // bit5 ce nonfinite, bit6 ce<=0
+    unsigned int row_status;           // bit0 some idx == -1, bit1 some idx == -2
+    int abort;                         // set by the scan kernel when validation failed
+    int range_bad;                     // k_max * h_max > 350
+};
+
+// Model classes for Workspace::model_err
+constexpr unsigned kModelNonfinite = 1u;
+constexpr unsigned kModelBad = 2u;
+
+struct ModelArgs {
+    int64_t M;
+    int N;
+    const double *h, *alpha, *beta, *rho;
+};
+
+struct ScanArgs {
+    ModelArgs mod;
+    const double *lam;
+    int64_t L;
+    const double *c;
+    int64_t V;
+    double *ct;        // [M][L]
+    int32_t *idx;      // [M][L] or nullptr
+    Workspace *ws;
+    unsigned grid_mask;  // Workspace::grid_err bits that invalidate the call (0x1F, 0x7F with C_e)
+};
+
+// Launchers (masw_kernels.cu).  Each returns the cudaError_t of its launch.
+cudaError_t launch_validate(const ModelArgs &m, const double *lam, int64_t L, const double *c,
+                            int64_t V, const double *ce, Workspace *ws, cudaStream_t st);
+cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device);
+cudaError_t launch_misfit(const double *ct, const double *ce, int64_t M, int64_t L,
+                          double *misfit, Workspace *ws, unsigned grid_mask, bool check_models,
+                          cudaStream_t st);
+cudaError_t launch_validate_ce(const double *ce, int64_t L, Workspace *ws, cudaStream_t st);
+cudaError_t launch_argmin(const double *misfit, int64_t M, int64_t *best, double *best_val,
+                          cudaStream_t st);
+cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, const double *c,
+                            int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
+                            cudaStream_t st);
+int auto_team_warps(int64_t rows, int64_t V, int device);
+
+void count_launch();
+long long launches();
+
+}  // namespace masw

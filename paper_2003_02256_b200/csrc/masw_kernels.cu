@@ -1,0 +1,513 @@
+// masw_kernels.cu -- sm_100a kernels of libmasw.so.
+//
+//   validate_kernel   argument checks of include/masw.h on device-resident inputs
+//   scan_kernel<TEAM> the hot path: persistent work-stealing kernel; a team of TEAM warps
+//                     takes one (model, lambda) row at a time and scans c upward in chunks
+//                     of 32*TEAM velocities; each lane assembles + eliminates one det in
+//                     registers (masw_det.cuh), signs are compared across lanes with
+//                     shuffles, the first change is found with a warp ballot (+ a shared-
+//                     memory min across the team's warps), and the team exits the row at
+//                     the first chunk that contains a change (Algorithm 1).
+//   misfit_kernel     Algorithm 2, one warp per model, fixed-order
+//                     butterfly sum (deterministic, independent of sharding).
+//   argmin_kernel     lowest misfit, ties -> lowest index.
+//   det_grid_kernel   debug/parity: every (lambda, c) det with mantissa/exponent.
+//
+// What differs from the paper's GPU design and why is in DESIGN.md:
+// no stiffness matrices in global memory, no separate assemble / eliminate / search / reduce
+// kernels, early exit instead of evaluating the whole grid, a work queue for
+// the load imbalance the paper repartitions for.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+
+#include "masw_det.cuh"
+#include "masw_internal.h"
+
+namespace masw {
+
+namespace {
+std::atomic<long long> g_launches{0};
+constexpr unsigned FULL = 0xffffffffu;
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launches() { return g_launches.load(std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------ validation
+
+__device__ __forceinline__ bool ws_range_bad(const Workspace *ws)
+{
+    // max_i,e fl(fl(2pi/lambda_i) * h_e) = fl(fl(2pi/lambda_min) * h_max): both roundings are
+    // monotone, so this is exactly the per-pair guard of include/masw.h.
+    const double lam_min = __longlong_as_double((long long)~ws->lam_min_nbits);
+    const double h_max = __longlong_as_double((long long)ws->h_max_bits);
+    const double kmax = kTwoPi / lam_min;
+    return kmax * h_max > kMaxKH;
+}
+
+// grid_mask selects which grid_err bits make the call invalid.
+__device__ __forceinline__ bool ws_invalid(const Workspace *ws, unsigned grid_mask,
+                                           bool check_models)
+{
+    if (ws->grid_err & grid_mask) return true;
+    if (check_models) {
+        if (ws->model_err != 0ull) return true;
+        if (ws_range_bad(ws)) return true;
+    }
+    return false;
+}
+
+__global__ void validate_kernel(ModelArgs m, const double *__restrict__ lam, int64_t L,
+                                const double *__restrict__ c, int64_t V,
+                                const double *__restrict__ ce, Workspace *ws)
+{
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned gerr = 0;
+    double lmin = INFINITY, hmax = 0.0;
+    if (lam) {
+        for (int64_t i = tid; i < L; i += stride) {
+            const double x = lam[i];
+            if (!isfinite(x)) gerr |= 1u;
+            else if (!(x > 0.0)) gerr |= 4u;
+            else lmin = fmin(lmin, x);
+        }
+    }
+    if (c) {
+        for (int64_t j = tid; j < V; j += stride) {
+            const double x = c[j];
+            if (!isfinite(x)) {
+                gerr |= 2u;
+            } else {
+                if (j == 0 && !(x > 0.0)) gerr |= 8u;
+                if (j > 0 && !(x > c[j - 1])) gerr |= 16u;
+            }
+        }
+    }
+    if (ce) {
+        for (int64_t i = tid; i < L; i += stride) {
+            const double x = ce[i];
+            if (!isfinite(x)) gerr |= 32u;
+            else if (!(x > 0.0)) gerr |= 64u;
+        }
+    }
+    const int N = m.N;
+    for (int64_t k = tid; k < m.M; k += stride) {
+        bool nonfinite = false, bad = false;
+        for (int e = 0; e < N; ++e) {
+            const double h = m.h[k * N + e];
+            nonfinite |= !isfinite(h);
+            bad |= !(h > 0.0);
+            if (isfinite(h)) hmax = fmax(hmax, h);
+        }
+        for (int e = 0; e <= N; ++e) {
+            const double a = m.alpha[k * (N + 1) + e], b = m.beta[k * (N + 1) + e],
+                         r = m.rho[k * (N + 1) + e];
+            nonfinite |= !isfinite(a) || !isfinite(b) || !isfinite(r);
+            bad |= !(r > 0.0) || !(b > 0.0) || !(a > b);
+        }
+        const unsigned cls = nonfinite ? kModelNonfinite : (bad ? kModelBad : 0u);
+        if (cls) atomicMax(&ws->model_err, ~(((unsigned long long)k << 2) | cls));
+    }
+    if (gerr) atomicOr(&ws->grid_err, gerr);
+    if (lmin < INFINITY)
+        atomicMax(&ws->lam_min_nbits, ~(unsigned long long)__double_as_longlong(lmin));
+    if (hmax > 0.0) atomicMax(&ws->h_max_bits, (unsigned long long)__double_as_longlong(hmax));
+}
+
+cudaError_t launch_validate(const ModelArgs &m, const double *lam, int64_t L, const double *c,
+                            int64_t V, const double *ce, Workspace *ws, cudaStream_t st)
+{
+    int64_t n = m.M;
+    if (L > n) n = L;
+    if (V > n) n = V;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks < 1) blocks = 1;
+    if (blocks > 1184) blocks = 1184;
+    validate_kernel<<<blocks, 256, 0, st>>>(m, lam, L, c, V, ce, ws);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_ce(const double *ce, int64_t L, Workspace *ws, cudaStream_t st)
+{
+    ModelArgs none{0, 1, nullptr, nullptr, nullptr, nullptr};
+    return launch_validate(none, nullptr, L, nullptr, 0, ce, ws, st);
+}
+
+// ------------------------------------------------------------------ scan
+
+template <int TEAM, int BLOCK>
+__device__ __forceinline__ void team_sync(int team)
+{
+    if constexpr (TEAM == 1) {
+        __syncwarp();
+    } else if constexpr (TEAM * 32 == BLOCK) {
+        __syncthreads();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TEAM * 32) : "memory");
+    }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// Shared memory: per team a control block then the row's LayerConst[N+1] and the
+// 2(N+1) layer velocities used by the perturbation rule.
+struct TeamCtrl {
+    long long row;
+    int first[2][32];
+    int last[2][32];
+};
+
+__host__ __device__ constexpr size_t round8(size_t x) { return (x + 7) & ~size_t(7); }
+
+__host__ __device__ inline size_t team_model_bytes(int N)
+{
+    return (size_t)(N + 1) * sizeof(LayerConst) + (size_t)2 * (N + 1) * sizeof(double);
+}
+
+template <int TEAM, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) scan_kernel(ScanArgs a)
+{
+    constexpr int TEAMS = BLOCK / (32 * TEAM);
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_abort;
+
+    const int N = a.mod.N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int team = warp / TEAM, wt = warp % TEAM, tl = wt * 32 + lane;
+
+    TeamCtrl *ctrl = reinterpret_cast<TeamCtrl *>(smem) + team;
+    unsigned char *mbase = smem + round8(sizeof(TeamCtrl) * TEAMS) + team * team_model_bytes(N);
+    LayerConst *lc = reinterpret_cast<LayerConst *>(mbase);
+    double *vel = reinterpret_cast<double *>(mbase + (size_t)(N + 1) * sizeof(LayerConst));
+
+    Workspace *ws = a.ws;
+    if (threadIdx.x == 0) {
+        const bool bad = ws_invalid(ws, a.grid_mask, true);
+        s_abort = bad;
+        if (bad && blockIdx.x == 0) ws->abort = 1;
+    }
+    __syncthreads();
+    if (s_abort) return;
+
+    const int64_t M = a.mod.M, L = a.L, V = a.V;
+    const int64_t rows = M * L;
+    const double *__restrict__ cg = a.c;
+    unsigned long long my_alg = 0, my_eval = 0;
+    unsigned my_status = 0;
+    int buf = 0;
+
+    for (;;) {
+        // ---- pop a row (work-stealing queue; rows i-major so long wavelengths go first
+        //      when lambda is given in the usual decreasing order)
+        long long row;
+        if constexpr (TEAM == 1) {
+            if (lane == 0) row = (long long)atomicAdd(&ws->queue, 1ull);
+            row = __shfl_sync(FULL, row, 0);
+        } else {
+            if (tl == 0) ctrl->row = (long long)atomicAdd(&ws->queue, 1ull);
+            team_sync<TEAM, BLOCK>(team);
+            row = ctrl->row;
+        }
+        if (row >= rows) break;
+        const int64_t i = row / M, m = row - i * M;
+
+        // ---- per-row constants into shared memory (reading S2: k = 2 pi / lambda)
+        const double k = kTwoPi / a.lam[i];
+        for (int e = tl; e <= N; e += 32 * TEAM) {
+            const double al = a.mod.alpha[m * (N + 1) + e];
+            const double be = a.mod.beta[m * (N + 1) + e];
+            const double rh = a.mod.rho[m * (N + 1) + e];
+            LayerConst x;
+            x.kh = (e < N) ? k * a.mod.h[m * N + e] : 0.0;
+            x.ia2 = 1.0 / (al * al);
+            x.ib2 = 1.0 / (be * be);
+            x.krho = k * rh;
+            x.mu = k * rh * be * be;
+            lc[e] = x;
+            vel[2 * e] = al;
+            vel[2 * e + 1] = be;
+        }
+        team_sync<TEAM, BLOCK>(team);
+
+        // ---- ascending scan in chunks of 32*TEAM velocities
+        int carry = 0;
+        bool found = false;
+        for (int64_t base = 0; base < V; base += 32 * TEAM) {
+            const int64_t j = base + tl;
+            int s = 0;
+            bool bad = false;
+            if (j < V) {
+                const DetOut d = det_K<false>(lc, vel, N, cg[j]);
+                s = d.sign;
+                bad = d.bad;
+                ++my_eval;
+            }
+            int sprev = __shfl_up_sync(FULL, s, 1);
+            int64_t first = -1;
+            if constexpr (TEAM == 1) {
+                if (lane == 0) sprev = carry;
+                const bool ev = (j < V) && (bad || (j > 0 && s != sprev));
+                const unsigned mask = __ballot_sync(FULL, ev);
+                if (mask) first = base + (__ffs(mask) - 1);
+                carry = __shfl_sync(FULL, s, 31);
+            } else {
+                if (lane == 31) ctrl->last[buf][wt] = s;
+                team_sync<TEAM, BLOCK>(team);
+                if (lane == 0) sprev = (wt == 0) ? carry : ctrl->last[buf][wt - 1];
+                const bool ev = (j < V) && (bad || (j > 0 && s != sprev));
+                const unsigned mask = __ballot_sync(FULL, ev);
+                if (lane == 0) ctrl->first[buf][wt] = mask ? wt * 32 + (__ffs(mask) - 1) : INT_MAX;
+                team_sync<TEAM, BLOCK>(team);
+                int f = INT_MAX;
+#pragma unroll
+                for (int w = 0; w < TEAM; ++w) f = min(f, ctrl->first[buf][w]);
+                if (f != INT_MAX) first = base + f;
+                carry = ctrl->last[buf][TEAM - 1];
+                buf ^= 1;
+            }
+            if (first >= 0) {
+                if (j == first) {
+                    const int64_t o = m * L + i;
+                    if (bad) {
+                        a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+                        if (a.idx) a.idx[o] = -2;
+                        my_status |= 2u;
+                    } else {
+                        a.ct[o] = cg[j];
+                        if (a.idx) a.idx[o] = (int32_t)j;
+                    }
+                    my_alg += (unsigned long long)(j + 1);
+                }
+                found = true;
+                break;
+            }
+        }
+        if (!found && tl == 0) {
+            const int64_t o = m * L + i;
+            a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+            if (a.idx) a.idx[o] = -1;
+            my_status |= 1u;
+            my_alg += (unsigned long long)V;
+        }
+    }
+
+    // ---- per-warp aggregation of the work counters (one atomic per warp)
+    my_alg = warp_sum_u64(my_alg);
+    my_eval = warp_sum_u64(my_eval);
+    my_status = __reduce_or_sync(FULL, my_status);
+    if (lane == 0) {
+        if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
+        if (my_eval) atomicAdd(&ws->eval_dets, my_eval);
+        if (my_status) atomicOr(&ws->row_status, my_status);
+    }
+}
+
+int auto_team_warps(int64_t rows, int64_t V, int device)
+{
+    // Minimise tail idle (~ resident_warps / (2 TEAM rows)) + speculation waste
+    // (~ 16 TEAM / dets_per_row) with dets_per_row ~ V/2:  TEAM* = sqrt(Wres d / (32 R)).
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const double wres = sms * 32.0;
+    const double d = (double)V / 2.0;
+    const double t = sqrt(wres * d / (32.0 * (double)(rows > 0 ? rows : 1)));
+    int team = 1;
+    while (team * 2 <= t && team < 32) team *= 2;
+    return team;
+}
+
+template <int TEAM, int BLOCK>
+static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
+{
+    constexpr int TEAMS = BLOCK / (32 * TEAM);
+    const size_t smem = round8(sizeof(TeamCtrl) * TEAMS) + TEAMS * team_model_bytes(a.mod.N);
+    auto kern = scan_kernel<TEAM, BLOCK>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t rows = a.mod.M * a.L;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = (rows + TEAMS - 1) / TEAMS;
+    if (need < blocks) blocks = need;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, BLOCK, smem, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device)
+{
+    switch (team_warps) {
+        case 1: return launch_scan_t<1, 256>(a, st, device);
+        case 2: return launch_scan_t<2, 256>(a, st, device);
+        case 4: return launch_scan_t<4, 256>(a, st, device);
+        case 8: return launch_scan_t<8, 256>(a, st, device);
+        case 16: return launch_scan_t<16, 512>(a, st, device);
+        case 32: return launch_scan_t<32, 1024>(a, st, device);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ------------------------------------------------------------------ misfit (Algorithm 2)
+
+__global__ void __launch_bounds__(256) misfit_kernel(const double *__restrict__ ct,
+                                                     const double *__restrict__ ce, int64_t M,
+                                                     int64_t L, double *__restrict__ out,
+                                                     const Workspace *ws, unsigned grid_mask,
+                                                     bool check_models)
+{
+    if (ws_invalid(ws, grid_mask, check_models)) return;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= M) return;
+    const double *row = ct + wid * L;
+    double s = 0.0;
+    bool inf = false;
+    for (int64_t i = lane; i < L; i += 32) {
+        const double x = row[i];
+        if (!isfinite(x)) inf = true;
+        else s += fabs(x - ce[i]) / ce[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    inf = __any_sync(FULL, inf);
+    if (lane == 0) out[wid] = inf ? INFINITY : s / (double)L;
+}
+
+cudaError_t launch_misfit(const double *ct, const double *ce, int64_t M, int64_t L,
+                          double *misfit, Workspace *ws, unsigned grid_mask, bool check_models,
+                          cudaStream_t st)
+{
+    const int64_t blocks = (M * 32 + 255) / 256;
+    misfit_kernel<<<(unsigned)blocks, 256, 0, st>>>(ct, ce, M, L, misfit, ws, grid_mask,
+                                                    check_models);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ argmin
+
+__global__ void __launch_bounds__(1024) argmin_kernel(const double *__restrict__ v, int64_t M,
+                                                      int64_t *best, double *best_val)
+{
+    __shared__ double sv[32];
+    __shared__ long long si[32];
+    double bv = INFINITY;
+    long long bi = -1;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+        double x = v[i];
+        if (isnan(x)) x = INFINITY;
+        if (bi < 0 || x < bv) {   // ascending i per thread: strict < keeps the lowest index
+            bv = x;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(FULL, bv, o);
+        const long long oi = __shfl_xor_sync(FULL, bi, o);
+        if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        sv[warp] = bv;
+        si[warp] = bi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        bv = lane < nw ? sv[lane] : INFINITY;
+        bi = lane < nw ? si[lane] : -1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(FULL, bv, o);
+            const long long oi = __shfl_xor_sync(FULL, bi, o);
+            if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            *best = bi;
+            if (best_val) *best_val = bv;
+        }
+    }
+}
+
+cudaError_t launch_argmin(const double *misfit, int64_t M, int64_t *best, double *best_val,
+                          cudaStream_t st)
+{
+    argmin_kernel<<<1, 1024, 0, st>>>(misfit, M, best, best_val);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ det grid (debug)
+
+__global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const double *lam,
+                                                       int64_t L, const double *c, int64_t V,
+                                                       double *mre, double *mim, int32_t *ex,
+                                                       const Workspace *ws)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (ws_invalid(ws, 0x1Fu, true)) return;
+    const int N = mod.N;
+    LayerConst *lc = reinterpret_cast<LayerConst *>(smem);
+    double *vel = reinterpret_cast<double *>(smem + (size_t)(N + 1) * sizeof(LayerConst));
+    const int64_t i = blockIdx.y;
+    const double k = kTwoPi / lam[i];
+    for (int e = threadIdx.x; e <= N; e += blockDim.x) {
+        const double al = mod.alpha[e], be = mod.beta[e], rh = mod.rho[e];
+        LayerConst x;
+        x.kh = (e < N) ? k * mod.h[e] : 0.0;
+        x.ia2 = 1.0 / (al * al);
+        x.ib2 = 1.0 / (be * be);
+        x.krho = k * rh;
+        x.mu = k * rh * be * be;
+        lc[e] = x;
+        vel[2 * e] = al;
+        vel[2 * e + 1] = be;
+    }
+    __syncthreads();
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= V) return;
+    const DetOut d = det_K<true>(lc, vel, N, c[j]);
+    const int64_t o = i * V + j;
+    mre[o] = d.mre;
+    mim[o] = d.mim;
+    ex[o] = d.e2;
+}
+
+cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, const double *c,
+                            int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
+                            cudaStream_t st)
+{
+    const size_t smem = team_model_bytes(m.N);
+    dim3 grid((unsigned)((V + 255) / 256), (unsigned)L);
+    det_grid_kernel<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace masw

@@ -1,0 +1,149 @@
+"""Multi-rank host logic of paper_2003_02256_b200.distributed on CPU (gloo, world_size 2).
+
+The per-rank compute is injected (the CPU oracle) so the sharding, padded all-gathers,
+inverse permutation and argmin are exercised without a GPU; on a GPU box the same code runs
+with the CUDA library over NCCL.  Also: the partition laws of PAPER.md:124 / SPEC.md:316.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synth
+from paper_2003_02256_b200 import distributed as D
+
+
+# ------------------------------------------------------------------ partition laws
+
+def test_partition_laws_exhaustive():
+    for W in range(1, 201):
+        for s in range(1, W + 1):
+            for strat in ("contiguous", "modular"):
+                p = D.partition_wavelengths(W, s, strat)
+                flat = sorted(i for part in p for i in part)
+                assert flat == list(range(W))                        # disjoint + covering
+                sizes = [len(x) for x in p]
+                assert max(sizes) - min(sizes) <= 1                   # balanced
+            if s <= 3:
+                assert D.partition_wavelengths(W, s, "contiguous")[0][0] == 0
+
+
+def test_partition_paper_examples():
+    assert [len(x) for x in D.partition_wavelengths(40, 3, "contiguous")] == [14, 13, 13]
+    assert D.partition_wavelengths(10, 3, "modular") == [[0, 3, 6, 9], [1, 4, 7], [2, 5, 8]]
+    assert D.partition_wavelengths(5, 1, "modular") == [[0, 1, 2, 3, 4]]
+    assert [len(x) for x in D.partition_wavelengths(40, 4, "modular")] == [10] * 4
+
+
+def test_shard_bounds_cover():
+    for M in (0, 1, 7, 100_000):
+        for G in (1, 2, 3, 8):
+            b = [D.shard_bounds(M, G, r) for r in range(G)]
+            assert b[0][0] == 0 and b[-1][1] == M
+            assert all(b[k][1] == b[k + 1][0] for k in range(G - 1))
+
+
+def test_modular_balances_decreasing_curve_better(orc):
+    """SPEC.md:628 / PAPER.md:206: on the variable-40 curve, s=4, the max/min per-worker
+    determinant count is lower under the modular partition than the contiguous one."""
+    w = synth.workload("maswaves")
+    m = w.models
+    st, ct, idx, nd = orc.curve(m.h[0], m.alpha[0], m.beta[0], m.rho[0], w.lam, w.c)
+    ratio = {}
+    for strat in ("contiguous", "modular"):
+        loads = [int(nd[p].sum()) for p in D.partition_wavelengths(40, 4, strat)]
+        ratio[strat] = max(loads) / min(loads)
+    assert ratio["modular"] < ratio["contiguous"]
+
+
+# ------------------------------------------------------------------ gloo, world_size 2
+
+def oracle_ops():
+    import oracle
+
+    def ens(h, a, b, r, lam, c, ce):
+        mods = synth.Models(h.numpy(), a.numpy(), b.numpy(), r.numpy())
+        o = oracle.ensemble(mods, lam.numpy(), c.numpy(), ce.numpy(), nthreads=2)
+        return (o["status"], torch.from_numpy(o["ct"]), torch.from_numpy(o["idx"]),
+                torch.from_numpy(o["misfit"]))
+
+    def cur(h, a, b, r, lam, c):
+        st, ct, idx, nd = oracle.curve(h.numpy(), a.numpy(), b.numpy(), r.numpy(), lam.numpy(),
+                                       c.numpy(), nthreads=2)
+        return st, torch.from_numpy(ct), torch.from_numpy(idx)
+
+    def misfit(ct, ce):
+        return oracle.misfit(ct.numpy(), ce.numpy())[1]
+
+    def argmin(v):
+        v = v.numpy()
+        i = int(np.argmin(np.where(np.isnan(v), np.inf, v)))
+        return np.array([i]), np.array([v[i]])
+
+    return D.Ops(ens, cur, misfit, argmin)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        ops = oracle_ops()
+        w = synth.workload("ensemble", M=13)
+        mods = w.models
+        t = lambda x: torch.from_numpy(np.ascontiguousarray(x))
+        out = D.ensemble_sharded((t(mods.h), t(mods.alpha), t(mods.beta), t(mods.rho)), t(w.lam),
+                                 t(w.c), t(w.ce), ops=ops)
+        c2 = synth.workload("maswaves")
+        m = c2.models
+        res = {}
+        for strat in ("modular", "contiguous"):
+            co = D.curve_sharded(tuple(t(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)), t(c2.lam),
+                                 t(c2.c), t(c2.ce), strategy=strat, ops=ops)
+            res[strat] = (co.ct.numpy().copy(), co.idx.numpy().copy(), co.misfit, co.status)
+        q.put((rank, out.ct.numpy().copy(), out.idx.numpy().copy(), out.misfit.numpy().copy(),
+               out.best, out.status, res))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced through the queue
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+
+
+def test_gloo_world2_matches_single_process(orc):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for o in outs:
+        assert not isinstance(o[1], str), o[2]
+    w = synth.workload("ensemble", M=13)
+    ref = orc.ensemble(w.models, w.lam, w.c, w.ce)
+    c2 = synth.workload("maswaves")
+    m = c2.models
+    st, cct, cidx, _ = orc.curve(m.h[0], m.alpha[0], m.beta[0], m.rho[0], c2.lam, c2.c)
+    cm = orc.misfit(cct, c2.ce)[1]
+    for rank, ct, idx, mis, best, status, res in outs:
+        assert np.array_equal(idx, ref["idx"]) and np.array_equal(ct, ref["ct"])   # bitwise
+        assert np.array_equal(mis, ref["misfit"]) and best == ref["best"]
+        assert status == ref["status"]
+        for strat, (gct, gidx, gmis, gst) in res.items():
+            assert np.array_equal(gidx, cidx) and np.array_equal(gct, cct), strat
+            assert gmis == cm and gst == st

@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU fp64 oracle on the same
+seeded inputs (synth/), element by element, under the rules of tests/parity.py.
+
+Small cases run the oracle in full; full-size cases (BASELINE.json configs at their real
+sizes, in the launch configuration bench.py times) compare sampled rows and properties.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+import masw_parity as parity
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def masw():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2003_02256_b200 as m
+
+    m.lib()
+    return m
+
+
+def dev(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def margs(models, k=0):
+    return (models.h[k], models.alpha[k], models.beta[k], models.rho[k])
+
+
+# ------------------------------------------------------------------ det grid parity (S15)
+
+@pytest.mark.parametrize("name", ["tiny", "maswaves", "maswaves_twin"])
+def test_det_grid_parity(masw, orc, name):
+    w = synth.workload(name)
+    a = margs(w.models)
+    gre, gim, gex = masw.masw_det_grid(*a, w.lam, w.c)
+    st, omant, oex, osts = orc.det_grid(*a, w.lam, w.c)
+    assert st == 0 and np.all(osts == 0)
+    gm = gre + 1j * gim
+    rel = parity.det_grid_rel_err(gm, gex, omant, oex)
+    dom = parity.det_domain(omant, oex, w.c, w.models.beta.min())
+    assert dom.sum() > 0.3 * dom.size
+    worst = float(np.nanmax(rel[dom]))
+    assert worst <= parity.DET_RTOL, worst
+    # mantissa normalisation of the ABI (max(|re|,|im|) in [0.5, 1))
+    t = np.maximum(np.abs(gre), np.abs(gim))
+    assert np.all((t >= 0.5) & (t < 1.0))
+    # signs of Re det agree wherever the det is not near a root
+    assert np.all(np.sign(gre)[dom] == np.sign(omant.real)[dom])
+
+
+def test_det_grid_parity_uniform_n10(masw, orc):
+    m = synth.uniform_model()
+    a = margs(m)
+    lam = np.array(synth.UNIFORM_TIERS)
+    c = synth.uniform_grid()[::7]
+    gre, gim, gex = masw.masw_det_grid(*a, lam, c)
+    st, omant, oex, _ = orc.det_grid(*a, lam, c)
+    rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
+    dom = parity.det_domain(omant, oex, c, m.beta.min())
+    assert float(np.nanmax(rel[dom])) <= parity.DET_RTOL
+
+
+# ------------------------------------------------------------------ C_t parity, one model
+
+@pytest.mark.parametrize("name", ["tiny", "maswaves", "maswaves_twin"])
+@pytest.mark.parametrize("team", [0, 1, 2, 4, 8, 16, 32])
+def test_curve_parity_small(masw, orc, name, team):
+    w = synth.workload(name)
+    a = margs(w.models)
+    st, ct, idx = masw.masw_curve(*a, w.lam, w.c, team_warps=team)
+    ost, oct_, oidx, ond = orc.curve(*a, w.lam, w.c)
+    assert st == ost == 0
+    ok, exact, one = parity.ct_acceptable(orc, a, w.lam, w.c, idx, oidx)
+    assert ok.all() and exact == len(w.lam)            # these configs have no near-root rows
+    assert np.array_equal(ct, oct_)
+    alg, ev = masw.masw_last_work()
+    assert alg == int(ond.sum()) and ev >= alg          # SPEC.md:246 early-exit count
+
+
+def test_curve_device_pointers_and_async(masw, orc):
+    w = synth.workload("maswaves")
+    a = margs(w.models)
+    st, ct, idx = masw.masw_curve(*[dev(x) for x in a], dev(w.lam), dev(w.c))
+    ost, oct_, oidx, _ = orc.curve(*a, w.lam, w.c)
+    assert st == 0 and torch.equal(idx.cpu(), torch.as_tensor(oidx))
+    st, ct2, idx2 = masw.masw_curve(*[dev(x) for x in a], dev(w.lam), dev(w.c), flags=masw.ASYNC)
+    torch.cuda.synchronize()
+    assert st == 0 and torch.equal(ct2, ct)
+    # on a non-default stream
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st, ct3, idx3 = masw.masw_curve(*[dev(x) for x in a], dev(w.lam), dev(w.c))
+    s.synchronize()
+    assert torch.equal(ct3, ct)
+
+
+def test_curve_wavelength_permutation(masw):
+    w = synth.workload("maswaves")
+    a = margs(w.models)
+    p = np.random.default_rng(3).permutation(len(w.lam))
+    _, ct, idx = masw.masw_curve(*a, w.lam, w.c)
+    _, ctp, idxp = masw.masw_curve(*a, w.lam[p], w.c)
+    assert np.array_equal(idxp, idx[p]) and np.array_equal(ctp, ct[p])
+
+
+def test_rayleigh_and_no_change_rows(masw, orc):
+    b = 200.0
+    al = b * math.sqrt(3.0)
+    st, ct, idx = masw.masw_curve([1.0], [al, al], [b, b], [1900.0, 1900.0], [5.0, 10.0, 20.0],
+                                  synth.maswaves_grid())
+    assert st == 0 and list(idx) == [367] * 3 and list(ct) == [184.0] * 3      # P1
+    st, ct, idx = masw.masw_curve([1.0], [al, al], [b, b], [1900.0, 1900.0], [5.0],
+                                  np.linspace(50, 150, 11))
+    assert st == masw.WARN_NO_SIGN_CHANGE and idx[0] == -1 and math.isnan(ct[0])
+    alg, ev = masw.masw_last_work()
+    assert alg == 11
+
+
+@pytest.mark.parametrize("N", [1, 3, 10, 24, 64])
+def test_identical_stack_any_depth(masw, N):
+    b = 200.0
+    al = b * math.sqrt(3.0)
+    h = np.full(N, 0.37)
+    st, ct, idx = masw.masw_curve(h, [al] * (N + 1), [b] * (N + 1), [1900.0] * (N + 1),
+                                  [5.0, 20.0], synth.maswaves_grid())
+    assert st == 0 and list(idx) == [367, 367]
+
+
+def test_error_codes_match_oracle(masw, orc):
+    g = synth.maswaves_grid()
+    m = synth.maswaves_model()
+    a = margs(m)
+    cases = [
+        (a, [1.0], g[::-1]),
+        (a, [-1.0], g),
+        (a, [0.01], g),
+        (a, [1.0], np.r_[0.0, g]),
+        (a, [np.nan], g),
+        ((a[0], a[1], a[1], a[3]), [1.0], g),      # alpha == beta
+        ((np.r_[0.0, a[0][1:]], a[1], a[2], a[3]), [1.0], g),
+    ]
+    for args, lam, c in cases:
+        ost = orc.curve(*args, lam, c)[0]
+        with pytest.raises(masw.MaswError) as ei:
+            masw.masw_curve(*args, lam, c)
+        assert ei.value.code == ost, (lam, ei.value.code, ost)
+    with pytest.raises(masw.MaswError) as ei:
+        masw.masw_curve(*a, [1.0], g[:1])
+    assert ei.value.code == masw.E_ARG
+    N = 65
+    with pytest.raises(masw.MaswError) as ei:
+        masw.masw_curve(np.ones(N), np.full(N + 1, 300.0), np.full(N + 1, 100.0), np.ones(N + 1),
+                        [10.0], g)
+    assert ei.value.code == masw.E_ARG
+    # outputs untouched on error
+    ct = np.full(1, 7.0)
+    idx = np.full(1, 9, dtype=np.int32)
+    with pytest.raises(masw.MaswError):
+        masw.masw_curve(*a, [1.0], g[::-1], ct_out=ct, idx_out=idx)
+    assert ct[0] == 7.0 and idx[0] == 9
+
+
+# ------------------------------------------------------------------ misfit / argmin
+
+def test_misfit_examples_and_errors(masw, orc):
+    assert masw.masw_misfit([110.0], [100.0]) == pytest.approx(0.10, abs=1e-15)
+    assert masw.masw_misfit([110.0, 90.0], [100.0, 100.0]) == pytest.approx(0.10, abs=1e-15)
+    assert masw.masw_misfit([np.nan, 1.0], [1.0, 1.0]) == math.inf
+    with pytest.raises(masw.MaswError) as ei:
+        masw.masw_misfit([1.0], [0.0])
+    assert ei.value.code == masw.E_ARG
+    with pytest.raises(masw.MaswError) as ei:
+        masw.masw_misfit([1.0], [np.inf])
+    assert ei.value.code == masw.E_NONFINITE
+    rng = np.random.default_rng(1)
+    ct = rng.uniform(50, 300, (37, 1234))
+    ce = rng.uniform(50, 300, 1234)
+    gm = masw.masw_misfit_batch(ct, ce)
+    for k in range(37):
+        assert parity.misfit_ok(orc, ct[k], ce, gm[k])
+
+
+def test_argmin_ties_and_nan(masw):
+    v = np.array([3.0, 1.0, 2.0, 1.0, np.nan, np.inf])
+    b, bv = masw.masw_argmin(v)
+    assert int(b[0]) == 1 and bv[0] == 1.0
+    v = np.full(100_001, np.inf)
+    v[77_777] = 0.5
+    v[99_999] = 0.5
+    b, bv = masw.masw_argmin(dev(v))
+    assert int(b.cpu()[0]) == 77_777
+    b, bv = masw.masw_argmin(np.full(5, np.inf))
+    assert int(b[0]) == 0
+
+
+# ------------------------------------------------------------------ ensembles
+
+def test_ensemble_parity_small(masw, orc):
+    w = synth.workload("ensemble", M=300)
+    mods = w.models
+    res = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, w.lam, w.c, w.ce)
+    o = orc.ensemble(mods, w.lam, w.c, w.ce)
+    assert res.status == o["status"]
+    bad = 0
+    for m in range(mods.n_models):
+        ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), w.lam, w.c, res.idx[m],
+                                              o["idx"][m])
+        assert ok.all()
+        bad += len(w.lam) - exact
+        assert parity.misfit_ok(orc, res.ct[m], w.ce, res.misfit[m])
+    assert bad <= 2
+    b, _ = masw.masw_argmin(res.misfit)
+    assert int(b[0]) == o["best"]
+
+
+def test_ensemble_team_and_pointer_kind_independence(masw):
+    w = synth.workload("ensemble", M=200)
+    mods = w.models
+    ref = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, w.lam, w.c, w.ce)
+    for team in (1, 2, 8, 32):
+        r = masw.masw_curves_ensemble(*[dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)],
+                                      dev(w.lam), dev(w.c), dev(w.ce), team_warps=team)
+        assert np.array_equal(r.idx.cpu().numpy(), ref.idx)
+        assert np.array_equal(r.misfit.cpu().numpy(), ref.misfit)   # bitwise: fixed-order sum
+
+
+def test_ensemble_edge_cases(masw, orc):
+    w = synth.workload("ensemble", M=3)
+    mods = w.models
+    r = masw.masw_curves_ensemble(mods.h[:0], mods.alpha[:0], mods.beta[:0], mods.rho[:0], w.lam,
+                                  w.c, w.ce)
+    assert r.status == 0 and r.ct.shape == (0, 40)
+    # L = 1, V = 2 (ragged everything)
+    r = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, w.lam[:1],
+                                  np.array([100.0, 400.0]), w.ce[:1])
+    o = orc.ensemble(mods, w.lam[:1], np.array([100.0, 400.0]), w.ce[:1])
+    assert np.array_equal(r.idx, o["idx"]) and r.status == o["status"]
+
+
+@pytest.mark.slow
+def test_ensemble_full_size_sampled(masw, orc):
+    """C5 at full size (100k models) through the device path bench.py times; the oracle
+    checks a seeded sample of models, the GPU's top-20 misfits, and the argmin."""
+    w = synth.workload("ensemble", M=100_000)
+    mods = w.models
+    res = masw.masw_curves_ensemble(*[dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)],
+                                    dev(w.lam), dev(w.c), dev(w.ce))
+    idx = res.idx.cpu().numpy()
+    ct = res.ct.cpu().numpy()
+    mis = res.misfit.cpu().numpy()
+    assert res.status in (0, 1)
+    rng = np.random.default_rng(200302256)
+    sample = np.unique(np.r_[rng.choice(100_000, 150, replace=False), np.argsort(mis)[:20],
+                             [0, 99_999]])
+    sub = mods.take(sample)
+    o = orc.ensemble(sub, w.lam, w.c, w.ce)
+    for k, m in enumerate(sample):
+        ok, exact, one = parity.ct_acceptable(orc, margs(sub, k), w.lam, w.c, idx[m], o["idx"][k])
+        assert ok.all(), m
+        assert parity.misfit_ok(orc, ct[m], w.ce, mis[m])
+    b, bv = masw.masw_argmin(res.misfit)
+    b = int(b.cpu()[0])
+    assert mis[b] == mis.min() and b == int(np.argmin(mis))
+    # the misfit of the argmin model recomputed by the oracle
+    ob = orc.ensemble(mods.take([b]), w.lam, w.c, w.ce)
+    assert ob["misfit"][0] <= mis[b] * (1 + 1e-9) + 1e-15
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tier", synth.UNIFORM_TIERS)
+def test_uniform_full_size(masw, orc, tier):
+    """C3: 10k identical wavelengths x 10k velocities, N=10; every row equals the oracle's
+    tier row (golden file written by scripts/make_golden.py from the oracle)."""
+    w = synth.workload("uniform", tier=tier)
+    a = margs(w.models)
+    st, ct, idx = masw.masw_curve(*[dev(x) for x in a], dev(w.lam), dev(w.c))
+    ct = ct.cpu().numpy()
+    want = synth.load_golden_tiers()[tier]
+    assert st == 0 and np.all(ct == want)
+
+
+@pytest.mark.slow
+def test_realistic_full_size(masw, orc):
+    """C4: 10k wavelengths 100 -> 0.5 m, 10k velocities; vs the oracle's golden curve."""
+    w = synth.workload("realistic")
+    a = margs(w.models)
+    st, ct, idx = masw.masw_curve(*[dev(x) for x in a], dev(w.lam), dev(w.c))
+    idx = idx.cpu().numpy()
+    golden_idx = np.array([int(l.split()[2]) for l in open(f"{synth.GOLDEN_DIR}/c4_ct_oracle.txt")
+                           if not l.startswith("#")])
+    ok, exact, one = parity.ct_acceptable(orc, a, w.lam, w.c, idx, golden_idx)
+    assert ok.all(), np.nonzero(~ok)[0][:10]
+    mis = masw.masw_misfit(ct, w.ce)
+    assert parity.misfit_ok(orc, ct.cpu().numpy(), w.ce, mis)
