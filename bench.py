@@ -1,0 +1,454 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the MASW forward model on B200 (driver contract, one JSON line).
+
+Workload (BASELINE.json configs[4]): the Monte-Carlo inversion ensemble,
+100,000 random 6-layer models x the paper's 40-wavelength "variable" curve x 1000 test
+velocities, against one experimental curve C_e.  One step = the whole hot path (§8(a) a1-a8):
+validate, scan every (model, lambda) row to its first sign change (assembly + banded
+determinant + ballot scan in one kernel), fused misfit per model, all-gather of C_t / idx /
+misfit over NCCL when sharded, and the argmin.  Models are sharded contiguously over ranks
+(strong scaling: the 100k total is fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+value      algorithmic determinants/s = sum over rows of (idx+1) / device time,
+           whole job, inputs resident in HBM, L2 flushed (256 MiB write) between steps.
+e2e        the same metric through the C ABI with pinned HOST buffers (H2D of the step's
+           inputs and D2H of C_t/idx/misfit inside the timed region).
+roofline   the scan kernel against the FP64 ALU peak.
+cpu_baseline / --impl reference: the CPU fp64 oracle (oracle/, test infrastructure) on the
+           host cores, on a bounded sample of the same ensemble.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "stiffness determinants/sec (algorithmic, early-exit count)"
+UNIT = "det/s"
+# SURVEY.md §8(d) per-determinant algorithmic flops: elimination 35N+30, assembly 40N
+# real + N divisions + 4N exp-class (2N cosh/sinh-or-cos/sin pairs), half-space 3.
+def flops_per_det(N: int) -> int:
+    return 35 * N + 30 + 40 * N + N + 4 * N + 3
+
+
+# FP64 ALU peak derived from the unit counts and clock (B200_PROFILING.md: 148 SMs,
+# clocks.max.sm 1965 MHz; 64 FP64 FMA lanes per SM per clock, 2 flops per FMA).
+def fp64_peak_tflops(mhz: float = 1965.0) -> float:
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ------------------------------------------------------------------ clocks sampling
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.path = f"/tmp/masw_clocks_{os.getpid()}.csv"
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
+        except Exception:
+            return out
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.strip() == "Active":
+                    reasons.add(n)
+        if sm:
+            loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+            out["sm_mhz"] = statistics.median(loaded)
+            out["sm_max_mhz"] = max(mx)
+            out["samples"] = len(sm)
+        out["reasons"] = sorted(reasons)
+        try:
+            os.remove(self.path)
+        except OSError:
+            pass
+        return out
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+
+def oracle_sample(models, lam, c, ce, target_s: float, nthreads: int, start: int = 0):
+    """Run the oracle on consecutive models from `start` until ~target_s of wall time.
+    Returns (n_models, alg_dets, seconds)."""
+    import oracle
+
+    oracle.build()
+    t0 = time.perf_counter()
+    done, dets = 0, 0
+    batch = max(1, nthreads)
+    M = models.n_models
+    while True:
+        lo = (start + done) % M
+        hi = min(lo + batch, M)
+        o = oracle.ensemble(models.slice(lo, hi), lam, c, ce, nthreads=nthreads)
+        dets += int(o["ndet"].sum())
+        done += hi - lo
+        el = time.perf_counter() - t0
+        if el >= target_s:
+            return done, dets, el
+        # grow batches so the loop overhead stays small
+        rate = done / el
+        batch = int(max(1, min(4 * batch, rate * (target_s - el) + 1)))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    w = synth.workload("ensemble", M=args.models)
+    cores = host_cores()
+    per_step = args.ref_step_seconds
+    # warm-up steps (untimed), then K timed steps, each a bounded sample of the ensemble
+    pos = 0
+    for _ in range(args.warmup):
+        n, _, _ = oracle_sample(w.models, w.lam, w.c, w.ce, min(per_step, 2.0), cores, pos)
+        pos += n
+    tot_n, tot_d, tot_s = 0, 0, 0.0
+    for _ in range(args.steps):
+        n, d, s = oracle_sample(w.models, w.lam, w.c, w.ce, per_step, cores, pos)
+        pos += n
+        tot_n += n
+        tot_d += d
+        tot_s += s
+    value = tot_d / tot_s
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args),
+        "curves_per_s": tot_n / tot_s,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{tot_n} consecutive models of the C5 ensemble over "
+                                   f"{args.steps} steps of ~{per_step:.0f} s "
+                                   f"(CPU: {cpu_model()})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args):
+    return {"workload": f"C5 Monte-Carlo ensemble: {args.models} random N=6 models x 40 "
+                        "wavelengths (variable curve) x 1000 test velocities, vs one C_e",
+            "models": args.models, "n_layers": 6, "wavelengths": 40, "velocities": 1000,
+            "sharding": "models, contiguous blocks per rank; NCCL all-gather of C_t/idx/misfit",
+            "l2": "flushed between timed steps (256 MiB write)",
+            "inputs": "seeded synthetic (synth.ensemble_models, PCG64 200302256)"}
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_02256_b200 as masw
+    from paper_2003_02256_b200 import distributed as D
+
+    rank, world, local = env_rank()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device(f"cuda:{torch.cuda.current_device()}")
+
+    w = synth.workload("ensemble", M=args.models)
+    mods = w.models
+    M, N = mods.h.shape
+    L, V = len(w.lam), len(w.c)
+    lo, hi = D.shard_bounds(M, world, rank)
+    counts = [D.shard_bounds(M, world, r)[1] - D.shard_bounds(M, world, r)[0] for r in range(world)]
+    Mr = hi - lo
+
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+    dh, da, db, dr = (t(x[lo:hi]) for x in (mods.h, mods.alpha, mods.beta, mods.rho))
+    dlam, dc, dce = t(w.lam), t(w.c), t(w.ce)
+    pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
+    hh, ha, hb, hr = (pin(x[lo:hi]) for x in (mods.h, mods.alpha, mods.beta, mods.rho))
+    hlam, hc, hce = pin(w.lam), pin(w.c), pin(w.ce)
+    ct = torch.empty((Mr, L), dtype=torch.float64, device=dev)
+    idx = torch.empty((Mr, L), dtype=torch.int32, device=dev)
+    mis = torch.empty((Mr,), dtype=torch.float64, device=dev)
+    hct = torch.empty((Mr, L), dtype=torch.float64).pin_memory()
+    hidx = torch.empty((Mr, L), dtype=torch.int32).pin_memory()
+    hmis = torch.empty((Mr,), dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    peak_probe = masw.masw_probe_fp64_peak(-1, 200.0)[0] if rank == 0 else None
+
+    def gather(x):
+        return D._all_gather_padded(x, counts) if world > 1 else x
+
+    def step_device():
+        r = masw.masw_curves_ensemble(dh, da, db, dr, dlam, dc, dce, ct_out=ct, idx_out=idx,
+                                      misfit_out=mis, flags=masw.TIME_SCAN)
+        alg, _ = masw.masw_last_work()
+        scan_ms = masw.masw_last_scan_ms()
+        ct_all, idx_all, mis_all = gather(ct), gather(idx), gather(mis)
+        best, bval = masw.masw_argmin(mis_all)
+        return alg, scan_ms, best
+
+    def step_e2e():
+        masw.masw_curves_ensemble(hh, ha, hb, hr, hlam, hc, hce, ct_out=hct, idx_out=hidx,
+                                  misfit_out=hmis)
+        alg, _ = masw.masw_last_work()
+        if world > 1:
+            mis_all = gather(hmis.to(dev, non_blocking=True))
+            best, bval = masw.masw_argmin(mis_all)
+            b = int(best.cpu()[0])
+        else:
+            best, bval = masw.masw_argmin(hmis)
+            b = int(best[0])
+        return alg, b
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        step_device()
+        step_e2e()
+    barrier()
+
+    # ---- timed device steps (inputs resident; L2 flushed between steps, outside the events)
+    launches0 = masw.masw_kernel_launches()
+    step_ms, scan_ms, algs = [], [], []
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    phys = int(vis[local]) if local < len(vis) and vis[local].strip().isdigit() else local
+    with ClockSampler(phys) as clk:
+        barrier()
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            alg, sms, _ = step_device()
+            e1.record()
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            scan_ms.append(sms)
+            algs.append(alg)
+        barrier()
+    launches = masw.masw_kernel_launches() - launches0
+    clocks = clk.summary()
+
+    # ---- timed e2e steps (host buffers through the C ABI)
+    e2e_ms = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step_e2e()
+        e1.record()
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    barrier()
+
+    # ---- max over ranks, job totals
+    tot = torch.tensor([sum(step_ms), sum(e2e_ms), sum(scan_ms)], dtype=torch.float64, device=dev)
+    dets = torch.tensor([float(sum(algs))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.all_reduce(dets, op=dist.ReduceOp.SUM)
+    dev_ms, e2e_tot_ms, _ = tot.tolist()
+    total_dets = dets.item()                     # all ranks, all K steps
+    value = total_dets / (dev_ms / 1e3)
+    e2e_value = total_dets / (e2e_tot_ms / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the scan kernel (rank 0's launches; algorithmic flops / kernel time)
+    F = flops_per_det(N)
+    my_dets_per_step = sum(algs) / args.steps
+    kern_ms = statistics.mean(scan_ms)
+    achieved = my_dets_per_step * F / (kern_ms / 1e3) / 1e12
+    peak = fp64_peak_tflops()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "scan_kernel_ncu.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_launch_scaled_to_bench")
+        except Exception:
+            traffic = None
+    h2d = sum(x.numel() * x.element_size() for x in (hh, ha, hb, hr, hlam, hc, hce))
+    d2h = sum(x.numel() * x.element_size() for x in (hct, hidx, hmis)) + 16
+    if world > 1:
+        h2d += hmis.numel() * 8
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded PCG64 ensemble, SURVEY.md §8(d) C5)",
+        "config": config_dict(args),
+        "curves_per_s": M * args.steps / (dev_ms / 1e3),
+        "dets_per_step": total_dets / args.steps,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_tot_ms / args.steps},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "scan_kernel<1,256> (fused assemble + banded GEPP det + ballot scan)",
+                     "kernel_ms": kern_ms, "flops_per_det": F,
+                     "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
+                                    "(B200_PROFILING.md counts; MEASURED_PEAKS.json has no FP64)",
+                     "peak_probe_dfma_tflops": peak_probe},
+        "clocks": clocks,
+    }
+    if not args.no_extra and world == 1:
+        line["other_configs"] = other_configs(masw, torch, dev)
+    if not args.no_cpu:
+        cores = host_cores()
+        n, d, s = oracle_sample(mods, w.lam, w.c, w.ce, args.cpu_seconds, cores)
+        line["cpu_baseline"] = {"value": d / s, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": f"first {n} models of the C5 ensemble "
+                                          f"({d} algorithmic dets in {s:.1f} s; CPU: {cpu_model()})",
+                                "curves_per_s": n / s}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def other_configs(masw, torch, dev):
+    """Single-curve configs C1-C4 on one GPU (device pointers): latency / throughput."""
+    out = {}
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+    for name, kw, reps in [("tiny", {}, 50), ("maswaves", {}, 50),
+                           ("uniform", {"tier": 200.0}, 5), ("realistic", {}, 5)]:
+        w = synth.workload(name, **kw)
+        m = w.models
+        args = [t(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)]
+        lam, c = t(w.lam), t(w.c)
+        for _ in range(3):
+            masw.masw_curve(*args, lam, c)
+        torch.cuda.synchronize()
+        ts, scans = [], []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            masw.masw_curve(*args, lam, c, flags=masw.TIME_SCAN)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+            scans.append(masw.masw_last_scan_ms())
+        alg, ev = masw.masw_last_work()
+        med = statistics.median(ts)
+        out[name] = {"call_ms_median": med, "scan_ms_median": statistics.median(scans),
+                     "dets": alg, "dets_per_s": alg / (med / 1e3),
+                     "curves_per_s": 1e3 / med, "note": w.note}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--models", type=int, default=100_000)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("bench.py: --warmup must be >= 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -100,7 +100,7 @@ typedef struct {
     int32_t device;        /* CUDA device ordinal; -1 = current device                      */
     void *cuda_stream;     /* cudaStream_t; NULL = legacy default stream                     */
     int32_t team_warps;    /* warps cooperating on one (model, lambda) row: 0 = auto, else a
-                              power of two in [1, 32]; each step scans 32*team_warps
+                              power of two in [1, 16]; each step scans 32*team_warps
                               consecutive velocities speculatively       */
     uint32_t flags;        /* MASW_* flags above                                             */
 } masw_exec;

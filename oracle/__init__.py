@@ -17,6 +17,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "masw_oracle.c")
+CORE = os.path.join(HERE, "masw_det_core.h")
 LIB = os.path.join(HERE, "libmasw_oracle.so")
 
 OK, WARN_NO_SIGN_CHANGE = 0, 1
@@ -33,7 +34,8 @@ _I64 = ctypes.POINTER(ctypes.c_int64)
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (plain -O2, no fast-math, no FMA contraction)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+    if (force or not os.path.exists(LIB) or
+            os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(CORE))):
         cmd = ["gcc", "-std=gnu11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
                "-shared", "-pthread", "-o", LIB + ".tmp", SRC, "-lm"]
         subprocess.check_call(cmd)
@@ -62,6 +64,10 @@ def lib():
             L.oracle_det_dense.argtypes = [ctypes.c_int32, _D, _D, _I32]
             L.oracle_det.argtypes = [ctypes.c_int32, _D, _D, _D, _D, ctypes.c_double,
                                      ctypes.c_double, _D, _I32]
+            L.oracle_det_ld.argtypes = L.oracle_det.argtypes
+            L.oracle_det_grid_ld.argtypes = [ctypes.c_int32, _D, _D, _D, _D, _D, ctypes.c_int64,
+                                             _D, ctypes.c_int64, _D, _D, _I32, _I32,
+                                             ctypes.c_int32]
             L.oracle_curve.argtypes = [ctypes.c_int32, _D, _D, _D, _D, _D, ctypes.c_int64, _D,
                                        ctypes.c_int64, _D, _I32, _I64, ctypes.c_int32]
             L.oracle_misfit.argtypes = [_D, _D, ctypes.c_int64, _D]
@@ -146,14 +152,16 @@ def det_dense(A: np.ndarray):
     return complex(m[0], m[1]), int(e.value), st
 
 
-def det(h, alpha, beta, rho, lam, c):
-    """O1–O5 at one (λ, c): returns (complex mantissa, exponent, status)."""
+def det(h, alpha, beta, rho, lam, c, extended: bool = False):
+    """O1–O5 at one (λ, c): returns (complex mantissa, exponent, status).
+
+    ``extended=True`` runs the same arithmetic in long double (reading S15' audit)."""
     N = len(h)
     args = [_d(x) for x in (h, alpha, beta, rho)]
     m = np.zeros(2)
     e = ctypes.c_int32(0)
-    st = lib().oracle_det(N, *[p for _, p in args], float(lam), float(c), m.ctypes.data_as(_D),
-                          ctypes.byref(e))
+    fn = lib().oracle_det_ld if extended else lib().oracle_det
+    st = fn(N, *[p for _, p in args], float(lam), float(c), m.ctypes.data_as(_D), ctypes.byref(e))
     return complex(m[0], m[1]), int(e.value), st
 
 
@@ -215,8 +223,10 @@ def ensemble(models, lam, c, ce=None, nthreads: int | None = None):
     return dict(status=st, ct=ct, idx=idx, misfit=mis, ndet=nd, best=int(best.value))
 
 
-def det_grid(h, alpha, beta, rho, lam, c, nthreads: int | None = None):
-    """O10: full (λ, c) det grid → (status, mant[L][V] complex, exp[L][V], status[L][V])."""
+def det_grid(h, alpha, beta, rho, lam, c, nthreads: int | None = None, extended: bool = False):
+    """O10: full (λ, c) det grid → (status, mant[L][V] complex, exp[L][V], status[L][V]).
+
+    ``extended=True``: the same grid carried in long double (reading S15' audit)."""
     N = len(h)
     args = [_d(x) for x in (h, alpha, beta, rho)]
     lam, plam = _d(lam)
@@ -226,7 +236,8 @@ def det_grid(h, alpha, beta, rho, lam, c, nthreads: int | None = None):
     mim = np.zeros((L, V))
     ex = np.zeros((L, V), dtype=np.int32)
     sts = np.zeros((L, V), dtype=np.int32)
-    st = lib().oracle_det_grid(N, *[p for _, p in args], plam, L, pc, V, mre.ctypes.data_as(_D),
+    fn = lib().oracle_det_grid_ld if extended else lib().oracle_det_grid
+    st = fn(N, *[p for _, p in args], plam, L, pc, V, mre.ctypes.data_as(_D),
                                mim.ctypes.data_as(_D), ex.ctypes.data_as(_I32),
                                sts.ctypes.data_as(_I32), nthreads or default_threads())
     return st, mre + 1j * mim, ex, sts

@@ -42,6 +42,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <tgmath.h>
 
 typedef double complex cplx;
 
@@ -135,47 +136,29 @@ double oracle_perturb_velocity(int32_t N, const double *alpha, const double *bet
     }
 }
 
-/* ------------------------------------------------------------------ O3 layer element
- * Kausel-Roesset / MASWaves layer stiffness (the paper cites the
- * method only, "stiffness matrix method (Kausel, 1981)"; reading S1).
- * Complex arithmetic throughout, principal square roots (reading S3):
- *   r = sqrt(1 - c^2/alpha^2), s = sqrt(1 - c^2/beta^2)
- *   Cr = cosh(k r h), Sr = sinh(k r h), Cs = cosh(k s h), Ss = sinh(k s h)
- *   D  = 2(1 - Cr Cs) + (1/(r s) + r s) Sr Ss,   f = k rho c^2 / D
- *   k11 = f (Cr Ss/s - r Sr Cs)          k12 = f (Cr Cs - r s Sr Ss - 1) - k rho beta^2 (1 + s^2)
- *   k13 = f (r Sr - Ss/s)                k14 = f (Cs - Cr)
- *   k22 = f (Sr Cs/r - s Cr Ss)          k24 = f (s Ss - Sr/r)
- *   Ke = [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12], [k14, k24, -k12, k22]]
- * Local DOFs (u_top, w_top, u_bot, w_bot).
+/* ------------------------------------------------------------------ O3-O5
+ * The element / assembly / dense-LU steps live in masw_det_core.h, instantiated for fp64
+ * (the oracle) and for long double (its rounding-error audit, reading S15').
  */
-static void layer_element(double h, double alpha, double beta, double rho, double k, double c,
-                          cplx Ke[4][4])
-{
-    cplx r = csqrt(1.0 - (c * c) / (alpha * alpha));
-    cplx s = csqrt(1.0 - (c * c) / (beta * beta));
-    cplx Cr = ccosh(k * r * h), Sr = csinh(k * r * h);
-    cplx Cs = ccosh(k * s * h), Ss = csinh(k * s * h);
-    cplx D = 2.0 * (1.0 - Cr * Cs) + (1.0 / (r * s) + r * s) * Sr * Ss;
-    cplx f = k * rho * c * c / D;
-    cplx k11 = f * (Cr * Ss / s - r * Sr * Cs);
-    cplx k12 = f * (Cr * Cs - r * s * Sr * Ss - 1.0) - k * rho * beta * beta * (1.0 + s * s);
-    cplx k13 = f * (r * Sr - Ss / s);
-    cplx k14 = f * (Cs - Cr);
-    cplx k22 = f * (Sr * Cs / r - s * Cr * Ss);
-    cplx k24 = f * (s * Ss - Sr / r);
-    cplx M[4][4] = {{k11, k12, k13, k14},
-                    {k12, k22, -k14, k24},
-                    {k13, -k14, k11, -k12},
-                    {k14, k24, -k12, k22}};
-    memcpy(Ke, M, sizeof(M));
-}
+#define REAL double
+#define SFX d
+#include "masw_det_core.h"
+#undef REAL
+#undef SFX
+#define REAL long double
+#define SFX ld
+#include "masw_det_core.h"
+#undef REAL
+#undef SFX
+
+typedef long double complex cplx_ld;
 
 /* Exported for the pins: Ke as 16 complex numbers, row-major, (re, im) interleaved. */
 void oracle_layer_element(double h, double alpha, double beta, double rho, double k, double c,
                           double *out32)
 {
     cplx Ke[4][4];
-    layer_element(h, alpha, beta, rho, k, c, Ke);
+    layer_element_d(h, alpha, beta, rho, k, c, Ke);
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
             out32[2 * (4 * a + b)] = creal(Ke[a][b]);
@@ -183,29 +166,11 @@ void oracle_layer_element(double h, double alpha, double beta, double rho, doubl
         }
 }
 
-/* ------------------------------------------------------------------ O4 half-space element
- *   K_hs = k rho beta^2 [[ r(1-s^2)/(1-rs),    (1-s^2)/(1-rs) - 2 ],
- *                        [ (1-s^2)/(1-rs) - 2, s(1-s^2)/(1-rs)    ]]
- * (reading S1, S22.)
- */
-static void halfspace_element(double alpha, double beta, double rho, double k, double c,
-                              cplx Kh[2][2])
-{
-    cplx r = csqrt(1.0 - (c * c) / (alpha * alpha));
-    cplx s = csqrt(1.0 - (c * c) / (beta * beta));
-    double mu = k * rho * beta * beta;
-    cplx q = (1.0 - s * s) / (1.0 - r * s);
-    Kh[0][0] = mu * r * q;
-    Kh[0][1] = mu * q - 2.0 * mu;
-    Kh[1][0] = Kh[0][1];
-    Kh[1][1] = mu * s * q;
-}
-
 void oracle_halfspace_element(double alpha, double beta, double rho, double k, double c,
                               double *out8)
 {
     cplx Kh[2][2];
-    halfspace_element(alpha, beta, rho, k, c, Kh);
+    halfspace_element_d(alpha, beta, rho, k, c, Kh);
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {
             out8[2 * (2 * a + b)] = creal(Kh[a][b]);
@@ -213,95 +178,17 @@ void oracle_halfspace_element(double alpha, double beta, double rho, double k, d
         }
 }
 
-/* Dense global assembly: layer e adds Ke into rows/cols 2e..2e+3, the half-space adds
- * K_hs into rows/cols 2N, 2N+1 (PAPER.md:78 order 2(N+1)).  c is used as
- * given (callers pass the perturbed c'). */
-static void assemble(int32_t N, const double *h, const double *alpha, const double *beta,
-                     const double *rho, double k, double c, cplx *K /* [n*n] */)
-{
-    int n = 2 * (N + 1);
-    for (int i = 0; i < n * n; ++i) K[i] = 0.0;
-    for (int e = 0; e < N; ++e) {
-        cplx Ke[4][4];
-        layer_element(h[e], alpha[e], beta[e], rho[e], k, c, Ke);
-        for (int a = 0; a < 4; ++a)
-            for (int b = 0; b < 4; ++b) K[(2 * e + a) * n + (2 * e + b)] += Ke[a][b];
-    }
-    cplx Kh[2][2];
-    halfspace_element(alpha[N], beta[N], rho[N], k, c, Kh);
-    for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b) K[(2 * N + a) * n + (2 * N + b)] += Kh[a][b];
-}
-
 void oracle_assemble(int32_t N, const double *h, const double *alpha, const double *beta,
                      const double *rho, double k, double c, double *out /* [n*n*2] */)
 {
     int n = 2 * (N + 1);
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
-    assemble(N, h, alpha, beta, rho, k, c, K);
+    assemble_d(N, h, alpha, beta, rho, k, c, K);
     for (int i = 0; i < n * n; ++i) {
         out[2 * i] = creal(K[i]);
         out[2 * i + 1] = cimag(K[i]);
     }
     free(K);
-}
-
-/* ------------------------------------------------------------------ O5 determinant
- * Dense LU with partial pivoting (row of largest |a_ik|).  det = (-1)^swaps * prod u_kk,
- * accumulated as mant * 2^exp2 with max(|Re mant|, |Im mant|) in [0.5, 1) (reading S14).
- * Returns OR_OK, or OR_E_NONFINITE if any entry or pivot is not finite.  An all-zero
- * pivot column gives det = 0 exactly (mant = 0, exp2 = 0).
- */
-static int det_lu(int n, cplx *A, cplx *mant, int *exp2)
-{
-    for (int i = 0; i < n * n; ++i)
-        if (!isfinite(creal(A[i])) || !isfinite(cimag(A[i]))) return OR_E_NONFINITE;
-    cplx m = 1.0;
-    int ex = 0;
-    for (int kk = 0; kk < n; ++kk) {
-        int p = kk;
-        double best = cabs(A[kk * n + kk]);
-        for (int i = kk + 1; i < n; ++i) {
-            double v = cabs(A[i * n + kk]);
-            if (v > best) {
-                best = v;
-                p = i;
-            }
-        }
-        if (best == 0.0) {
-            *mant = 0.0;
-            *exp2 = 0;
-            return OR_OK;
-        }
-        if (p != kk) {
-            for (int j = 0; j < n; ++j) {
-                cplx t = A[kk * n + j];
-                A[kk * n + j] = A[p * n + j];
-                A[p * n + j] = t;
-            }
-            m = -m;
-        }
-        cplx piv = A[kk * n + kk];
-        for (int i = kk + 1; i < n; ++i) {
-            cplx l = A[i * n + kk] / piv;
-            for (int j = kk; j < n; ++j) A[i * n + j] -= l * A[kk * n + j];
-        }
-        m *= piv;
-        double t = fmax(fabs(creal(m)), fabs(cimag(m)));
-        if (!isfinite(t)) return OR_E_NONFINITE;
-        if (t == 0.0) {
-            *mant = 0.0;
-            *exp2 = 0;
-            return OR_OK;
-        }
-        int e2;
-        frexp(t, &e2);
-        m = ldexp(creal(m), -e2) + I * ldexp(cimag(m), -e2);
-        ex += e2;
-    }
-    *mant = m;
-    *exp2 = ex;
-    return OR_OK;
 }
 
 /* Exported for the pins: determinant of a dense complex matrix ((re, im) interleaved). */
@@ -311,22 +198,12 @@ int oracle_det_dense(int32_t n, const double *a /* [n*n*2] */, double *mant2, in
     for (int i = 0; i < n * n; ++i) A[i] = a[2 * i] + I * a[2 * i + 1];
     cplx m = 0.0;
     int e = 0;
-    int st = det_lu(n, A, &m, &e);
+    int st = det_lu_d(n, A, &m, &e);
     free(A);
     mant2[0] = creal(m);
     mant2[1] = cimag(m);
     *exp2 = e;
     return st;
-}
-
-/* O1-O5 for one (model, lambda, c): k, perturb, assemble, dense det. */
-static int det_at(int32_t N, const double *h, const double *alpha, const double *beta,
-                  const double *rho, double lambda, double c, cplx *K, cplx *mant, int *exp2)
-{
-    double k = OR_TWO_PI / lambda;
-    double cp = oracle_perturb_velocity(N, alpha, beta, c);
-    assemble(N, h, alpha, beta, rho, k, cp, K);
-    return det_lu(2 * (N + 1), K, mant, exp2);
 }
 
 int oracle_det(int32_t N, const double *h, const double *alpha, const double *beta,
@@ -336,10 +213,26 @@ int oracle_det(int32_t N, const double *h, const double *alpha, const double *be
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
     cplx m = 0.0;
     int e = 0;
-    int st = det_at(N, h, alpha, beta, rho, lambda, c, K, &m, &e);
+    int st = det_at_d(N, h, alpha, beta, rho, lambda, c, K, &m, &e);
     free(K);
     mant2[0] = creal(m);
     mant2[1] = cimag(m);
+    *exp2 = e;
+    return st;
+}
+
+/* The same determinant carried in long double (reading S15'): mantissa rounded to double. */
+int oracle_det_ld(int32_t N, const double *h, const double *alpha, const double *beta,
+                  const double *rho, double lambda, double c, double *mant2, int32_t *exp2)
+{
+    int n = 2 * (N + 1);
+    cplx_ld *K = (cplx_ld *)malloc(sizeof(cplx_ld) * n * n);
+    cplx_ld m = 0.0;
+    int e = 0;
+    int st = det_at_ld(N, h, alpha, beta, rho, lambda, c, K, &m, &e);
+    free(K);
+    mant2[0] = (double)creall(m);
+    mant2[1] = (double)cimagl(m);
     *exp2 = e;
     return st;
 }
@@ -367,7 +260,7 @@ static void scan_row(int32_t N, const double *h, const double *alpha, const doub
     for (int64_t j = 0; j < V; ++j) {
         cplx m = 0.0;
         int e;
-        int st = det_at(N, h, alpha, beta, rho, lambda, c[j], K, &m, &e);
+        int st = det_at_d(N, h, alpha, beta, rho, lambda, c[j], K, &m, &e);
         ++count;
         if (st != OR_OK) {
             *idx = OR_IDX_NONFINITE;
@@ -562,6 +455,7 @@ typedef struct {
     int64_t L, V;
     double *mre, *mim;
     int32_t *ex, *status;
+    int extended; /* 1: long double audit instance (reading S15') */
     atomic_llong next;
 } grid_job;
 
@@ -570,28 +464,64 @@ static void *grid_worker(void *arg)
     grid_job *G = (grid_job *)arg;
     int n = 2 * (G->N + 1);
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    cplx_ld *Kl = (cplx_ld *)malloc(sizeof(cplx_ld) * n * n);
     for (;;) {
         int64_t i = atomic_fetch_add(&G->next, 1);
         if (i >= G->L) break;
         for (int64_t j = 0; j < G->V; ++j) {
-            cplx m = 0.0;
-            int e = 0;
-            int st = det_at(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], K, &m, &e);
+            double re, im;
+            int e = 0, st;
+            if (G->extended) {
+                cplx_ld m = 0.0;
+                st = det_at_ld(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], Kl, &m, &e);
+                re = (double)creall(m);
+                im = (double)cimagl(m);
+            } else {
+                cplx m = 0.0;
+                st = det_at_d(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], K, &m, &e);
+                re = creal(m);
+                im = cimag(m);
+            }
             int64_t o = i * G->V + j;
-            G->mre[o] = creal(m);
-            G->mim[o] = cimag(m);
+            G->mre[o] = re;
+            G->mim[o] = im;
             G->ex[o] = e;
             if (G->status) G->status[o] = st;
         }
     }
     free(K);
+    free(Kl);
     return NULL;
 }
+
+static int det_grid_impl(int extended, int32_t N, const double *h, const double *alpha,
+                         const double *beta, const double *rho, const double *lam, int64_t L,
+                         const double *c, int64_t V, double *mant_re, double *mant_im,
+                         int32_t *exp2, int32_t *status, int32_t nthreads);
 
 int oracle_det_grid(int32_t N, const double *h, const double *alpha, const double *beta,
                     const double *rho, const double *lam, int64_t L, const double *c, int64_t V,
                     double *mant_re, double *mant_im, int32_t *exp2, int32_t *status,
                     int32_t nthreads)
+{
+    return det_grid_impl(0, N, h, alpha, beta, rho, lam, L, c, V, mant_re, mant_im, exp2,
+                         status, nthreads);
+}
+
+/* The grid in long double (reading S15': measures the fp64 oracle's rounding error). */
+int oracle_det_grid_ld(int32_t N, const double *h, const double *alpha, const double *beta,
+                       const double *rho, const double *lam, int64_t L, const double *c,
+                       int64_t V, double *mant_re, double *mant_im, int32_t *exp2,
+                       int32_t *status, int32_t nthreads)
+{
+    return det_grid_impl(1, N, h, alpha, beta, rho, lam, L, c, V, mant_re, mant_im, exp2,
+                         status, nthreads);
+}
+
+static int det_grid_impl(int extended, int32_t N, const double *h, const double *alpha,
+                         const double *beta, const double *rho, const double *lam, int64_t L,
+                         const double *c, int64_t V, double *mant_re, double *mant_im,
+                         int32_t *exp2, int32_t *status, int32_t nthreads)
 {
     int st = validate_all(1, N, h, alpha, beta, rho, lam, L, c, V);
     if (st != OR_OK) return st;
@@ -599,6 +529,7 @@ int oracle_det_grid(int32_t N, const double *h, const double *alpha, const doubl
     G.N = N; G.h = h; G.alpha = alpha; G.beta = beta; G.rho = rho;
     G.lam = lam; G.c = c; G.L = L; G.V = V;
     G.mre = mant_re; G.mim = mant_im; G.ex = exp2; G.status = status;
+    G.extended = extended;
     atomic_init(&G.next, 0);
     if (nthreads <= 1) {
         grid_worker(&G);

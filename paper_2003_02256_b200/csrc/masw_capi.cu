@@ -179,7 +179,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
     if (mod_in.M == 0) return MASW_OK;
     t_last_alg = t_last_eval = -1;
     const Exec ex = resolve(exp);
-    if (ex.team != 0 && (ex.team < 1 || ex.team > 32 || (ex.team & (ex.team - 1))))
+    if (ex.team != 0 && (ex.team < 1 || ex.team > 16 || (ex.team & (ex.team - 1))))
         return MASW_E_ARG;
     int pdev = -1;
     const int kind = common_kind({mod_in.h, mod_in.alpha, mod_in.beta, mod_in.rho, lam, c, ce,

@@ -323,7 +323,7 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
     const double d = (double)V / 2.0;
     const double t = sqrt(wres * d / (32.0 * (double)(rows > 0 ? rows : 1)));
     int team = 1;
-    while (team * 2 <= t && team < 32) team *= 2;
+    while (team * 2 <= t && team < 16) team *= 2;
     return team;
 }
 
@@ -361,7 +361,6 @@ cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int 
         case 4: return launch_scan_t<4, 256>(a, st, device);
         case 8: return launch_scan_t<8, 256>(a, st, device);
         case 16: return launch_scan_t<16, 512>(a, st, device);
-        case 32: return launch_scan_t<32, 1024>(a, st, device);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -2,6 +2,9 @@
 
   * det K within 1e-9 relative (complex), inside the det-parity domain:
         c_j >= 0.5 * beta_min  and  |det_o| >= 1e-12 * max_row |det_o|           (S15)
+        and the fp64 oracle agrees with its own long-double instance to 1e-10  (S15')
+    (S15': where fp64 evaluation of the formula is itself uncertain above 1e-10, two fp64
+    implementations cannot be compared at 1e-9.)
   * C_t: the same grid index as the oracle, except where the oracle's |Re det| at the
     straddling points falls below 1e-12 of its scan maximum; there one step is allowed (S16).
   * misfit within 1e-9 relative of oracle_misfit(GPU C_t, C_e)                      (S13)
@@ -11,6 +14,7 @@ import math
 import numpy as np
 
 DET_RTOL = 1e-9
+AUDIT_RTOL = 1e-10
 NEAR_ROOT = 1e-12
 MISFIT_RTOL = 1e-9
 
@@ -27,12 +31,17 @@ def det_grid_rel_err(g_mant, g_exp, o_mant, o_exp):
         return np.abs(g - o_mant) / np.abs(o_mant)
 
 
-def det_domain(o_mant, o_exp, c, beta_min):
-    """Boolean mask of the det-parity domain (S15) on an [L][V] oracle grid."""
+def det_domain(o_mant, o_exp, c, beta_min, ld_mant=None, ld_exp=None):
+    """Boolean mask of the det-parity domain (S15, and S15' when the long-double audit grid
+    of the oracle is given) on an [L][V] oracle grid."""
     logabs = np.log2(np.abs(o_mant)) + o_exp
     rowmax = np.max(np.where(np.isfinite(logabs), logabs, -np.inf), axis=1, keepdims=True)
     big = logabs >= rowmax + math.log2(NEAR_ROOT)
-    return big & (c[None, :] >= 0.5 * beta_min)
+    dom = big & (c[None, :] >= 0.5 * beta_min)
+    if ld_mant is not None:
+        audit = det_grid_rel_err(o_mant, o_exp, ld_mant, ld_exp)
+        dom &= audit <= AUDIT_RTOL
+    return dom
 
 
 def ct_acceptable(orc, model_args, lam, c, idx_g, idx_o):

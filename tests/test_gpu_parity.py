@@ -44,9 +44,10 @@ def test_det_grid_parity(masw, orc, name):
     gre, gim, gex = masw.masw_det_grid(*a, w.lam, w.c)
     st, omant, oex, osts = orc.det_grid(*a, w.lam, w.c)
     assert st == 0 and np.all(osts == 0)
+    _, lmant, lex, _ = orc.det_grid(*a, w.lam, w.c, extended=True)
     gm = gre + 1j * gim
     rel = parity.det_grid_rel_err(gm, gex, omant, oex)
-    dom = parity.det_domain(omant, oex, w.c, w.models.beta.min())
+    dom = parity.det_domain(omant, oex, w.c, w.models.beta.min(), lmant, lex)
     assert dom.sum() > 0.3 * dom.size
     worst = float(np.nanmax(rel[dom]))
     assert worst <= parity.DET_RTOL, worst
@@ -64,15 +65,37 @@ def test_det_grid_parity_uniform_n10(masw, orc):
     c = synth.uniform_grid()[::7]
     gre, gim, gex = masw.masw_det_grid(*a, lam, c)
     st, omant, oex, _ = orc.det_grid(*a, lam, c)
+    _, lmant, lex, _ = orc.det_grid(*a, lam, c, extended=True)
     rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
-    dom = parity.det_domain(omant, oex, c, m.beta.min())
+    dom = parity.det_domain(omant, oex, c, m.beta.min(), lmant, lex)
+    assert dom.mean() > 0.5
     assert float(np.nanmax(rel[dom])) <= parity.DET_RTOL
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_det_parity_random_ensemble_points(masw, orc, seed):
+    """Det parity on random C5 models at random (lambda, c): 20 models x 40 lambda x 256 c."""
+    w = synth.workload("ensemble", M=400)
+    rng = np.random.default_rng(seed)
+    worst, n = 0.0, 0
+    for mi in rng.choice(400, 20, replace=False):
+        a = margs(w.models, mi)
+        c = np.sort(rng.uniform(0.5 * a[2].min(), 500.0, 256))
+        gre, gim, gex = masw.masw_det_grid(*a, w.lam, c)
+        st, omant, oex, _ = orc.det_grid(*a, w.lam, c)
+        _, lmant, lex, _ = orc.det_grid(*a, w.lam, c, extended=True)
+        rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
+        dom = parity.det_domain(omant, oex, c, a[2].min(), lmant, lex)
+        worst = max(worst, float(np.nanmax(rel[dom])))
+        n += int(dom.sum())
+    assert n > 0.8 * 20 * 40 * 256
+    assert worst <= parity.DET_RTOL, worst
 
 
 # ------------------------------------------------------------------ C_t parity, one model
 
 @pytest.mark.parametrize("name", ["tiny", "maswaves", "maswaves_twin"])
-@pytest.mark.parametrize("team", [0, 1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("team", [0, 1, 2, 4, 8, 16])
 def test_curve_parity_small(masw, orc, name, team):
     w = synth.workload(name)
     a = margs(w.models)
@@ -226,7 +249,7 @@ def test_ensemble_team_and_pointer_kind_independence(masw):
     w = synth.workload("ensemble", M=200)
     mods = w.models
     ref = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, w.lam, w.c, w.ce)
-    for team in (1, 2, 8, 32):
+    for team in (1, 2, 8, 16):
         r = masw.masw_curves_ensemble(*[dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)],
                                       dev(w.lam), dev(w.c), dev(w.ce), team_warps=team)
         assert np.array_equal(r.idx.cpu().numpy(), ref.idx)
@@ -299,5 +322,5 @@ def test_realistic_full_size(masw, orc):
                            if not l.startswith("#")])
     ok, exact, one = parity.ct_acceptable(orc, a, w.lam, w.c, idx, golden_idx)
     assert ok.all(), np.nonzero(~ok)[0][:10]
-    mis = masw.masw_misfit(ct, w.ce)
+    mis = masw.masw_misfit(ct, dev(w.ce))
     assert parity.misfit_ok(orc, ct.cpu().numpy(), w.ce, mis)

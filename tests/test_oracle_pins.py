@@ -279,13 +279,15 @@ def test_P8_no_sign_change_and_zero_sign(orc):
 
 # ------------------------------------------------------------------ P9 fp64 conditioning (mpmath)
 
-def _mp_det(h, alpha, beta, rho, lam, c, dps=50):
+def _mp_det(h, alpha, beta, rho, lam, c, dps=50, k_double=False):
+    """60-digit det K from App. A (bounds rounding, not the formula).  ``k_double`` uses the
+    fp64 wavenumber fl(2π/λ) exactly, so only arithmetic rounding differs from fp64 codes."""
     import mpmath as mp
 
     mp.mp.dps = dps
     N = len(h)
     n = 2 * (N + 1)
-    k = 2 * mp.pi / mp.mpf(lam)
+    k = mp.mpf(6.283185307179586 / lam) if k_double else 2 * mp.pi / mp.mpf(lam)
     c = mp.mpf(c)
     K = mp.matrix(n, n)
 
@@ -332,6 +334,37 @@ def test_P9_conditioning_envelope(orc, lam):
         want = _mp_det(*args, lam, c)
         rel = abs(got - want) / abs(want)
         assert rel < 1e-9, (lam, c, float(rel))
+
+
+def test_P9_extended_audit_is_accurate(orc):
+    """The long-double instance of the oracle's det path (reading S15') reproduces a
+    50-digit evaluation at the same fp64 inputs to 1e-11, including points where the fp64
+    oracle itself is off by ~1e-9 (so it can serve as the fp64 rounding-error audit)."""
+    w = synth.workload("ensemble", M=400)
+    mods = w.models
+    pts = [(313, 0, 30.554), (230, 17, 232.810), (286, 39, 23.157), (146, 7, 32.414),
+           (54, 16, 354.939), (121, 32, 244.121)]
+    worst_fp64 = 0.0
+    for mi, i, c in pts:
+        a = (mods.h[mi], mods.alpha[mi], mods.beta[mi], mods.rho[mi])
+        cp = orc.perturb_velocity(a[1], a[2], c)
+        ex = complex(_mp_det(*a, w.lam[i], cp, k_double=True))
+        ml, el, st = orc.det(*a, w.lam[i], c, extended=True)
+        assert st == 0 and abs(ml * 2.0 ** el - ex) <= 1e-11 * abs(ex)
+        m, e, st = orc.det(*a, w.lam[i], c)
+        worst_fp64 = max(worst_fp64, abs(m * 2.0 ** e - ex) / abs(ex))
+    assert worst_fp64 > 1e-10      # the audit matters: fp64 alone is not 1e-10-accurate here
+
+
+def test_P9_extended_grid_matches_pointwise(orc):
+    w = synth.workload("tiny")
+    m = w.models
+    a = (m.h[0], m.alpha[0], m.beta[0], m.rho[0])
+    st, mant, ex, sts = orc.det_grid(*a, w.lam[:3], w.c[::50], extended=True)
+    for i in range(3):
+        for j, c in enumerate(w.c[::50]):
+            mm, ee, s = orc.det(*a, w.lam[i], c, extended=True)
+            assert mm == mant[i, j] and ee == ex[i, j]
 
 
 # ------------------------------------------------------------------ P11 curve asymptotes
