@@ -21,6 +21,7 @@ using namespace masw;
 namespace {
 
 thread_local char t_cuda_err[256] = "";
+thread_local Workspace *t_pinned_ws = nullptr;   // pinned host copy target for the status read
 thread_local double t_last_scan_ms = -1.0;
 thread_local long long t_last_alg = -1, t_last_eval = -1;
 
@@ -141,6 +142,16 @@ struct Arena {
     }
 };
 
+// Reads the device workspace into pinned host memory (pageable copies can stall) and
+// synchronises the stream.
+Workspace read_status(const Workspace *ws, cudaStream_t st)
+{
+    if (!t_pinned_ws) CK(cudaMallocHost(&t_pinned_ws, sizeof(Workspace)));
+    CK(cudaMemcpyAsync(t_pinned_ws, ws, sizeof(Workspace), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return *t_pinned_ws;
+}
+
 // Error precedence of include/masw.h from the workspace filled by validate_kernel.
 int decode(const Workspace &w, bool with_ce, bool with_models)
 {
@@ -236,9 +247,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
             }
             return MASW_OK;
         }
-        Workspace w;
-        CK(cudaMemcpyAsync(&w, ws, sizeof(Workspace), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        const Workspace w = read_status(ws, st);
         if (timed) {
             float ms = -1.0f;
             CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -291,9 +300,7 @@ int run_misfit(const double *ct, const double *ce, int64_t M, int64_t L, double 
         CK(launch_validate_ce(dce, L, ws, st));
         CK(launch_misfit(dct, dce, M, L, dout, ws, 0x60u, false, st));
         if (!host && (ex.flags & MASW_ASYNC)) return MASW_OK;
-        Workspace w;
-        CK(cudaMemcpyAsync(&w, ws, sizeof(Workspace), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        const Workspace w = read_status(ws, st);
         const int code = decode(w, true, false);
         if (code < 0) return code;
         if (host) {
@@ -431,9 +438,7 @@ int masw_det_grid(const masw_model *model, const double *lambda, int64_t L, cons
         CK(launch_validate(mod, dlam, L, dc, V, nullptr, ws, st));
         CK(launch_det_grid(mod, dlam, L, dc, V, dre, dim, dex, ws, st));
         if (!host && (ex.flags & MASW_ASYNC)) return MASW_OK;
-        Workspace w;
-        CK(cudaMemcpyAsync(&w, ws, sizeof(Workspace), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        const Workspace w = read_status(ws, st);
         const int code = decode(w, false, true);
         if (code < 0) return code;
         if (host) {

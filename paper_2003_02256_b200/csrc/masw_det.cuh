@@ -46,60 +46,190 @@ struct LayerConst {
 };
 static_assert(sizeof(LayerConst) == 40, "LayerConst layout");
 
-// -------------------------------------------------------------- wave triple
-// cosh/sinh of th >= 0.  Small arguments use the Taylor series (no cancellation in
-// sinh ~ th, reading "Transcendental accuracy"); large ones exp and 1/exp.
+// -------------------------------------------------------------- fp64 elementary functions
+// Written for this kernel's argument ranges (all inputs finite and normal; see each function)
+// so that none of them needs the special-case branches of the general libm routines, and
+// with polynomial coefficients in the constant bank (DFMA takes them as c[][] operands; the
+// libm versions spend two UMOV issue slots per coefficient).  Each is within ~1-2 ulp.
+//
+// Taylor coefficients 1/k!, k = 0..20, correctly rounded.
+static __constant__ double c_invfact[21] = {
+    1.0, 1.0, 1.0 / 2.0, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0,
+    1.0 / 40320.0, 1.0 / 362880.0, 1.0 / 3628800.0, 1.0 / 39916800.0, 1.0 / 479001600.0,
+    1.0 / 6227020800.0, 1.0 / 87178291200.0, 1.0 / 1307674368000.0, 1.0 / 20922789888000.0,
+    1.0 / 355687428096000.0, 1.0 / 6402373705728000.0, 1.0 / 121645100408832000.0,
+    1.0 / 2432902008176640000.0};
+
+constexpr double kShifter = 6755399441055744.0;         // 1.5 * 2^52: round-to-integer trick
+constexpr double kLog2e = 1.4426950408889634;
+constexpr double kLn2Hi = 6.93147180369123816490e-01;   // ln 2 split (fdlibm)
+constexpr double kLn2Lo = 1.90821492927058770002e-10;
+constexpr double kTwoOverPi = 6.36619772367581382433e-01;
+constexpr double kPio2_1 = 1.57079632673412561417e+00;  // pi/2 split in 33+33+53 bits
+constexpr double kPio2_2 = 6.07710050650619224932e-11;  // (exact n*pio2_1 for n < 2^20)
+constexpr double kPio2_3 = 2.02226624879595063154e-21;
+
+// 1/x for finite normal x: MUFU approximation + two Newton steps (0 -> NaN, caught as bad).
+__device__ __forceinline__ double rcp_fast(double x)
+{
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
+// 1/sqrt(q) for finite q > 0: MUFU approximation + two Newton steps.
+__device__ __forceinline__ double rsqrt_fast(double q)
+{
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+    double h = 0.5 * y;
+    double e = fma(-q * y, y, 1.0);
+    y = fma(h, e, y);
+    h = 0.5 * y;
+    e = fma(-q * y, y, 1.0);
+    return fma(h, e, y);
+}
+
+// sqrt(q) and 1/sqrt(q) for finite q > 0: the refined reciprocal root plus one
+// residual correction of the root (x = x0 + (q - x0^2) / (2 x0)), ~0.5 ulp like IEEE sqrt.
+__device__ __forceinline__ void sqrt_rsqrt(double q, double &x, double &rx)
+{
+    rx = rsqrt_fast(q);
+    const double x0 = q * rx;
+    const double res = fma(-x0, x0, q);
+    x = fma(0.5 * rx, res, x0);
+}
+
+// x * 2^k by exponent arithmetic (no overflow/underflow for the ranges used here).
+__device__ __forceinline__ double scale2(double x, int k)
+{
+    return __hiloint2double(__double2hiint(x) + (k << 20), __double2loint(x));
+}
+
+// cosh and sinh of th in [0, 700]; the caller guarantees th <= 350 (range guard S9).
+// Below 1 the Taylor series (no cancellation in sinh); above, exp and 1/exp, where
+// sinh = A - B loses at most a factor coth(1) = 1.31.
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
 {
-    if (th < 0.5) {
+    if (th < 1.0) {
+        // sinh(t)/t = sum t^{2n}/(2n+1)!, n <= 9 (truncation < 1e-17 for t < 1);
+        // cosh(t) = sum t^{2n}/(2n)!, n <= 10 (truncation < 5e-19).
         const double t2 = th * th;
-        // sinh(t)/t = sum t^{2n}/(2n+1)!, n <= 7: truncation < 5e-17 for t < 0.5
-        double ps = 1.0 / 1307674368000.0;                 // 1/15!
-        ps = fma(ps, t2, 1.0 / 6227020800.0);              // 1/13!
-        ps = fma(ps, t2, 1.0 / 39916800.0);                // 1/11!
-        ps = fma(ps, t2, 1.0 / 362880.0);                  // 1/9!
-        ps = fma(ps, t2, 1.0 / 5040.0);                    // 1/7!
-        ps = fma(ps, t2, 1.0 / 120.0);                     // 1/5!
-        ps = fma(ps, t2, 1.0 / 6.0);                       // 1/3!
+        double ps = c_invfact[19];
+        ps = fma(ps, t2, c_invfact[17]);
+        ps = fma(ps, t2, c_invfact[15]);
+        ps = fma(ps, t2, c_invfact[13]);
+        ps = fma(ps, t2, c_invfact[11]);
+        ps = fma(ps, t2, c_invfact[9]);
+        ps = fma(ps, t2, c_invfact[7]);
+        ps = fma(ps, t2, c_invfact[5]);
+        ps = fma(ps, t2, c_invfact[3]);
         ps = fma(ps, t2, 1.0);
-        // cosh(t) = sum t^{2n}/(2n)!, n <= 8: truncation < 1e-18
-        double pc = 1.0 / 20922789888000.0;                // 1/16!
-        pc = fma(pc, t2, 1.0 / 87178291200.0);             // 1/14!
-        pc = fma(pc, t2, 1.0 / 479001600.0);               // 1/12!
-        pc = fma(pc, t2, 1.0 / 3628800.0);                 // 1/10!
-        pc = fma(pc, t2, 1.0 / 40320.0);                   // 1/8!
-        pc = fma(pc, t2, 1.0 / 720.0);                     // 1/6!
-        pc = fma(pc, t2, 1.0 / 24.0);                      // 1/4!
-        pc = fma(pc, t2, 0.5);                             // 1/2!
+        double pc = c_invfact[20];
+        pc = fma(pc, t2, c_invfact[18]);
+        pc = fma(pc, t2, c_invfact[16]);
+        pc = fma(pc, t2, c_invfact[14]);
+        pc = fma(pc, t2, c_invfact[12]);
+        pc = fma(pc, t2, c_invfact[10]);
+        pc = fma(pc, t2, c_invfact[8]);
+        pc = fma(pc, t2, c_invfact[6]);
+        pc = fma(pc, t2, c_invfact[4]);
+        pc = fma(pc, t2, 0.5);
         pc = fma(pc, t2, 1.0);
         sh = th * ps;
         ch = pc;
     } else {
-        const double e = exp(th);
-        const double ie = 1.0 / e;
-        ch = 0.5 * (e + ie);
-        sh = 0.5 * (e - ie);
+        // th = n ln2 + r, |r| <= ln2/2; e^r by its Taylor series to r^13 (< 5e-18);
+        // e^-r = 1/e^r with e^r in [0.7, 1.42]; cosh, sinh = 2^(n-1) e^r +- 2^(-n-1) e^-r.
+        const double t = fma(th, kLog2e, kShifter);
+        const double nd = t - kShifter;
+        const int n = __double2loint(t);
+        double r = fma(nd, -kLn2Hi, th);
+        r = fma(nd, -kLn2Lo, r);
+        double p = c_invfact[13];
+        p = fma(p, r, c_invfact[12]);
+        p = fma(p, r, c_invfact[11]);
+        p = fma(p, r, c_invfact[10]);
+        p = fma(p, r, c_invfact[9]);
+        p = fma(p, r, c_invfact[8]);
+        p = fma(p, r, c_invfact[7]);
+        p = fma(p, r, c_invfact[6]);
+        p = fma(p, r, c_invfact[5]);
+        p = fma(p, r, c_invfact[4]);
+        p = fma(p, r, c_invfact[3]);
+        p = fma(p, r, 0.5);
+        p = fma(p, r, 1.0);
+        p = fma(p, r, 1.0);
+        const double q = rcp_fast(p);
+        const double A = scale2(p, n - 1), B = scale2(q, -n - 1);
+        ch = A + B;
+        sh = A - B;
     }
 }
 
+// sin and cos of th in [0, 2^19 * pi/2) (Cody-Waite reduction, Taylor on |r| <= pi/4:
+// sin to r^15, cos to r^16, truncation < 1e-16).  Larger arguments use libm.
+__device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
+{
+    if (th >= 8.0e5) {
+        sincos(th, &sn, &cs);
+        return;
+    }
+    const double t = fma(th, kTwoOverPi, kShifter);
+    const double nd = t - kShifter;
+    const int n = __double2loint(t);
+    double r = fma(nd, -kPio2_1, th);
+    r = fma(nd, -kPio2_2, r);
+    r = fma(nd, -kPio2_3, r);
+    const double r2 = r * r;
+    double ps = -c_invfact[15];
+    ps = fma(ps, r2, c_invfact[13]);
+    ps = fma(ps, r2, -c_invfact[11]);
+    ps = fma(ps, r2, c_invfact[9]);
+    ps = fma(ps, r2, -c_invfact[7]);
+    ps = fma(ps, r2, c_invfact[5]);
+    ps = fma(ps, r2, -c_invfact[3]);
+    const double s = fma(r * r2, ps, r);
+    double pc = c_invfact[16];
+    pc = fma(pc, r2, -c_invfact[14]);
+    pc = fma(pc, r2, c_invfact[12]);
+    pc = fma(pc, r2, -c_invfact[10]);
+    pc = fma(pc, r2, c_invfact[8]);
+    pc = fma(pc, r2, -c_invfact[6]);
+    pc = fma(pc, r2, c_invfact[4]);
+    pc = fma(pc, r2, -0.5);
+    const double c = fma(r2, pc, 1.0);
+    // quadrant n mod 4: (sin, cos) = (s, c), (c, -s), (-s, -c), (-c, s)
+    const bool swap = n & 1;
+    const unsigned sgn_s = ((unsigned)n & 2u) << 30;         // sign bit for sin
+    const unsigned sgn_c = ((unsigned)(n + 1) & 2u) << 30;   // sign bit for cos
+    const double a = swap ? c : s;
+    const double b = swap ? s : c;
+    sn = __hiloint2double((int)((unsigned)__double2hiint(a) ^ sgn_s), __double2loint(a));
+    cs = __hiloint2double((int)((unsigned)__double2hiint(b) ^ sgn_c), __double2loint(b));
+}
+
+// -------------------------------------------------------------- wave triple
 // (C, XS, SX) for q = 1 - c^2/v^2 != 0 and kh = k*h.  See header comment.
 __device__ __forceinline__ void wave_triple(double q, double kh, double &C, double &XS,
                                             double &SX)
 {
     if (q > 0.0) {
-        const double rq = rsqrt(q);   // 1/x
-        const double x = q * rq;      // x
+        double x, rq;                      // x, 1/x
+        sqrt_rsqrt(q, x, rq);
         double ch, sh;
         cosh_sinh(kh * x, ch, sh);
         C = ch;
         XS = x * sh;
         SX = sh * rq;
     } else {
-        const double nq = -q;
-        const double rq = rsqrt(nq);  // 1/xi
-        const double xi = nq * rq;    // xi
+        double xi, rq;                     // xi, 1/xi
+        sqrt_rsqrt(-q, xi, rq);
         double sn, cs;
-        sincos(kh * xi, &sn, &cs);
+        sin_cos(kh * xi, sn, cs);
         C = cs;
         XS = -xi * sn;
         SX = sn * rq;
@@ -141,7 +271,7 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
     wave_triple(qb, L.kh, Cs, XSs, SXs);
     const double CC = Cr * Cs;
     const double D = fma(SXr, SXs, fma(XSr, XSs, 2.0 * (1.0 - CC)));
-    const double f = (L.krho * c2) / D;
+    const double f = (L.krho * c2) * rcp_fast(D);
     Elem E;
     E.k11 = f * fma(Cr, SXs, -XSr * Cs);
     E.k12 = fma(f, fma(-XSr, XSs, CC - 1.0), -L.mu * (1.0 + qb));
@@ -173,97 +303,105 @@ struct DetOut {
     int e2;        // det = (mre + i mim) * 2^e2 (only when WANT_VALUE)
 };
 
-template <int NC>
-__device__ __forceinline__ double sel4(int p, const double (&R)[4][NC], int c)
-{
-    return p == 0 ? R[0][c] : (p == 1 ? R[1][c] : (p == 2 ? R[2][c] : R[3][c]));
-}
-
+// -------------------------------------------------------------- banded GEPP step
 // One step of banded Gaussian elimination with partial pivoting over the 4 rows that can
-// hold nonzeros in the current node's two columns (reading S10/S11: 2 leftover rows of the
-// previous node + the 2 rows of the next node).  Columns: [node t | node t+1 | node t+2].
-// The pivot for each column is the row of largest magnitude (first in row order on ties),
-// exactly as dense GEPP picks it (the oracle), because every other row of K is
-// zero in these columns.  Rows are not moved: the pivot row is read through a select and
-// every other live row is updated with multiplier l_i (l = 0 for used rows).  The two rows
-// left over are returned in row order as the next step's first two rows.
-// parity = parity of the permutation (p, q, rest...) of the four rows.
-template <int NC, int NR>
-__device__ __forceinline__ void gepp_step(double (&R)[4][NC], double (&Ri)[4][NC], double &piv0,
-                                          double &piv1, int &parity, double (&X)[2][NC - 2],
-                                          double (&Xi)[2][NC - 2])
+// hold nonzeros in the current node's two columns (reading S10/S11): rows R[0], R[1] are the
+// two rows left by the previous step (matrix positions 2t, 2t+1), R[2], R[3] the two rows
+// of the next node (positions 2t+2, 2t+3); columns are [node t | node t+1 | node t+2].
+// Every other row of K is zero in these columns, so choosing the largest |entry| among the
+// four (first in position order on ties) and swapping it to the top is exactly the pivot
+// sequence of dense GEPP on K -- the oracle's algorithm.
+//
+// The pivot rows are resolved by BRANCHING on (p, q) into statically indexed code instead
+// of selecting rows through the index: along a warp's 32 consecutive velocities the pivot
+// pattern is uniform in ~90% of (chunk, step) pairs (measured on C5), so the branches are
+// mostly convergent and no per-element select instructions are issued.  NR = number of
+// trailing complex columns (2 in the last step, whose node-N columns carry K_hs).
+struct StepOut {
+    double piv0, piv1;
+    int parity;   // parity of the two GEPP row swaps
+};
+
+template <int NC, int NR, int P, int Q>
+__device__ __forceinline__ void gepp_finish(double (&R)[4][NC], double (&Ri)[4][NC],
+                                            StepOut &o, double (&X)[2][NC - 2],
+                                            double (&Xi)[2][NC - 2])
 {
-    // ---- column 0
-    int p = 0;
-    double best = fabs(R[0][0]);
-#pragma unroll
-    for (int i = 1; i < 4; ++i) {
-        const double a = fabs(R[i][0]);
-        if (a > best) {
-            best = a;
-            p = i;
-        }
-    }
-    piv0 = sel4<NC>(p, R, 0);
-    const double inv0 = (piv0 != 0.0) ? 1.0 / piv0 : 0.0;
-    double PR[NC], PRi[NC];
-#pragma unroll
-    for (int c = 1; c < NC; ++c) {
-        PR[c] = sel4<NC>(p, R, c);
-        if (c >= NC - NR) PRi[c] = sel4<NC>(p, Ri, c);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double l = (i == p) ? 0.0 : R[i][0] * inv0;
-#pragma unroll
-        for (int c = 1; c < NC; ++c) {
-            R[i][c] = fma(-l, PR[c], R[i][c]);
-            if (c >= NC - NR) Ri[i][c] = fma(-l, PRi[c], Ri[i][c]);
-        }
-    }
-    // ---- column 1 (rows other than p)
-    int q = -1;
-    best = -1.0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double a = (i == p) ? -1.0 : fabs(R[i][1]);
-        if (a > best) {
-            best = a;
-            q = i;
-        }
-    }
-    piv1 = sel4<NC>(q, R, 1);
-    const double inv1 = (piv1 != 0.0) ? 1.0 / piv1 : 0.0;
+    // positions after swap(0, P): pos[1..3]; after swap(1, Q): leftover = positions 2, 3
+    constexpr int pos1 = (P == 1) ? 0 : 1;
+    constexpr int pos2 = (P == 2) ? 0 : 2;
+    constexpr int pos3 = (P == 3) ? 0 : 3;
+    constexpr int prow = (Q == 1) ? pos1 : (Q == 2 ? pos2 : pos3);   // column-1 pivot row
+    constexpr int lo = (Q == 2) ? pos1 : pos2;
+    constexpr int hi = (Q == 3) ? pos1 : pos3;
+    o.piv1 = R[prow][1];
+    const double inv1 = (o.piv1 != 0.0) ? rcp_fast(o.piv1) : 0.0;
+    const double l_lo = R[lo][1] * inv1, l_hi = R[hi][1] * inv1;
 #pragma unroll
     for (int c = 2; c < NC; ++c) {
-        PR[c] = sel4<NC>(q, R, c);
-        if (c >= NC - NR) PRi[c] = sel4<NC>(q, Ri, c);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double l = (i == p || i == q) ? 0.0 : R[i][1] * inv1;
-#pragma unroll
-        for (int c = 2; c < NC; ++c) {
-            R[i][c] = fma(-l, PR[c], R[i][c]);
-            if (c >= NC - NR) Ri[i][c] = fma(-l, PRi[c], Ri[i][c]);
-        }
-    }
-    // ---- the two leftover rows, in row order
-    const int lo = (p != 0 && q != 0) ? 0 : ((p != 1 && q != 1) ? 1 : 2);
-    const int hi = (p != 3 && q != 3) ? 3 : ((p != 2 && q != 2) ? 2 : 1);
-#pragma unroll
-    for (int c = 2; c < NC; ++c) {
-        X[0][c - 2] = sel4<NC>(lo, R, c);
-        X[1][c - 2] = sel4<NC>(hi, R, c);
+        X[0][c - 2] = fma(-l_lo, R[prow][c], R[lo][c]);
+        X[1][c - 2] = fma(-l_hi, R[prow][c], R[hi][c]);
         if (c >= NC - NR) {
-            Xi[0][c - 2] = sel4<NC>(lo, Ri, c);
-            Xi[1][c - 2] = sel4<NC>(hi, Ri, c);
+            Xi[0][c - 2] = fma(-l_lo, Ri[prow][c], Ri[lo][c]);
+            Xi[1][c - 2] = fma(-l_hi, Ri[prow][c], Ri[hi][c]);
         } else {
             Xi[0][c - 2] = 0.0;
             Xi[1][c - 2] = 0.0;
         }
     }
-    parity = (p + q - (p < q ? 1 : 0)) & 1;
+    o.parity = (P != 0) ^ (Q != 1);
+}
+
+template <int NC, int NR, int P>
+__device__ __forceinline__ void gepp_after_p(double (&R)[4][NC], double (&Ri)[4][NC],
+                                             StepOut &o, double (&X)[2][NC - 2],
+                                             double (&Xi)[2][NC - 2])
+{
+    o.piv0 = R[P][0];
+    const double inv0 = (o.piv0 != 0.0) ? rcp_fast(o.piv0) : 0.0;
+    // eliminate column 0 from the three other rows with pivot row P
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (i == P) continue;
+        const double l = R[i][0] * inv0;
+#pragma unroll
+        for (int c = 1; c < NC; ++c) {
+            R[i][c] = fma(-l, R[P][c], R[i][c]);
+            if (c >= NC - NR) Ri[i][c] = fma(-l, Ri[P][c], Ri[i][c]);
+        }
+    }
+    // column-1 pivot among positions 1..3 (rows pos1, pos2, pos3), first max wins
+    constexpr int pos1 = (P == 1) ? 0 : 1;
+    constexpr int pos2 = (P == 2) ? 0 : 2;
+    constexpr int pos3 = (P == 3) ? 0 : 3;
+    const double b1 = fabs(R[pos1][1]), b2 = fabs(R[pos2][1]), b3 = fabs(R[pos3][1]);
+    if (b2 > b1 && b2 >= b3) {
+        gepp_finish<NC, NR, P, 2>(R, Ri, o, X, Xi);
+    } else if (b3 > b1 && b3 > b2) {
+        gepp_finish<NC, NR, P, 3>(R, Ri, o, X, Xi);
+    } else {
+        gepp_finish<NC, NR, P, 1>(R, Ri, o, X, Xi);
+    }
+}
+
+template <int NC, int NR>
+__device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4][NC],
+                                             double (&X)[2][NC - 2], double (&Xi)[2][NC - 2])
+{
+    StepOut o;
+    const double a0 = fabs(R[0][0]), a1 = fabs(R[1][0]), a2 = fabs(R[2][0]), a3 = fabs(R[3][0]);
+    int p = 0;
+    double best = a0;
+    if (a1 > best) { best = a1; p = 1; }
+    if (a2 > best) { best = a2; p = 2; }
+    if (a3 > best) { best = a3; p = 3; }
+    switch (p) {
+        case 0: gepp_after_p<NC, NR, 0>(R, Ri, o, X, Xi); break;
+        case 1: gepp_after_p<NC, NR, 1>(R, Ri, o, X, Xi); break;
+        case 2: gepp_after_p<NC, NR, 2>(R, Ri, o, X, Xi); break;
+        default: gepp_after_p<NC, NR, 3>(R, Ri, o, X, Xi); break;
+    }
+    return o;
 }
 
 // Determinant of K(k, c) for one row whose LayerConst[0..N] and velocity list are in `lc`,
@@ -279,11 +417,14 @@ __device__ __forceinline__ void gepp_step(double (&R)[4][NC], double (&Ri)[4][NC
 // (reading S3/S5), so the pivots and all but the last node's columns are real fp64; only
 // node N's columns (K_hs) are complex.  det K = (-1)^parity * prod pivots * det(last 2x2).
 // Cost per node: one layer element + one 4-row GEPP step, O(N) in total.
+// `maybe_near` = false asserts that no layer velocity lies within 1e-3 of c (the scan
+// decides it once per warp for its 32 velocities), which skips the per-lane S4 loop exactly.
 template <bool WANT_VALUE>
 __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
-                                        const double *__restrict__ vel, int N, double c)
+                                        const double *__restrict__ vel, int N, double c,
+                                        bool maybe_near = true)
 {
-    const double cp = perturb_velocity(vel, 2 * (N + 1), c);
+    const double cp = maybe_near ? perturb_velocity(vel, 2 * (N + 1), c) : c;
     const double c2 = cp * cp;
 
     int neg = 0, perm = 0;
@@ -303,9 +444,9 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
             {P.k14, P.k24, Q.k12 - P.k12, P.k22 + Q.k22, -Q.k14, Q.k24}};
         double Ri[4][6];   // unused (real step): NR = 0
         double Xi[2][4];
-        double piv0, piv1;
-        int par;
-        gepp_step<6, 0>(R, Ri, piv0, piv1, par, X, Xi);
+        const StepOut so = gepp_step<6, 0>(R, Ri, X, Xi);
+        const double piv0 = so.piv0, piv1 = so.piv1;
+        const int par = so.parity;
         neg ^= par ^ (piv0 < 0.0) ^ (piv1 < 0.0);
         perm ^= par;
         zero |= (piv0 == 0.0) | (piv1 == 0.0);
@@ -325,21 +466,21 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
         const double qa = fma(-c2, ia2, 1.0), qb = fma(-c2, ib2, 1.0);
         const double w = c2 * ib2;
         if (qb > 0.0) {                     // c < beta_N < alpha_N: r, s real
-            const double r = sqrt(qa), s = sqrt(qb);
-            const double g = mu * (w / (1.0 - r * s));
+            const double r = qa * rsqrt_fast(qa), s = qb * rsqrt_fast(qb);
+            const double g = mu * (w * rcp_fast(1.0 - r * s));
             h11r = r * g; h11i = 0.0;
             h12r = g - 2.0 * mu; h12i = 0.0;
             h22r = s * g; h22i = 0.0;
         } else if (qa > 0.0) {              // beta_N < c < alpha_N: r real, s = i xs
-            const double r = sqrt(qa), xs = sqrt(-qb);
+            const double r = qa * rsqrt_fast(qa), xs = -qb * rsqrt_fast(-qb);
             const double t = r * xs;        // 1/(1 - i t) = (1 + i t)/(1 + t^2)
-            const double gre = mu * (w / fma(t, t, 1.0)), gim = gre * t;
+            const double gre = mu * (w * rcp_fast(fma(t, t, 1.0))), gim = gre * t;
             h11r = r * gre; h11i = r * gim;
             h12r = gre - 2.0 * mu; h12i = gim;
             h22r = -xs * gim; h22i = xs * gre;
         } else {                            // c > alpha_N: r = i xr, s = i xs
-            const double xr = sqrt(-qa), xs = sqrt(-qb);
-            const double g = mu * (w / fma(xr, xs, 1.0));
+            const double xr = -qa * rsqrt_fast(-qa), xs = -qb * rsqrt_fast(-qb);
+            const double g = mu * (w * rcp_fast(fma(xr, xs, 1.0)));
             h11r = 0.0; h11i = xr * g;
             h12r = g - 2.0 * mu; h12i = 0.0;
             h22r = 0.0; h22i = xs * g;
@@ -356,9 +497,9 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
                        {0.0, 0.0, h11i, h12i},
                        {0.0, 0.0, h12i, h22i}};
     double Y[2][2], Yi[2][2];
-    double piv0, piv1;
-    int par;
-    gepp_step<4, 2>(R, Ri, piv0, piv1, par, Y, Yi);
+    const StepOut so = gepp_step<4, 2>(R, Ri, Y, Yi);
+    const double piv0 = so.piv0, piv1 = so.piv1;
+    const int par = so.parity;
     neg ^= par ^ (piv0 < 0.0) ^ (piv1 < 0.0);
     perm ^= par;
     zero |= (piv0 == 0.0) | (piv1 == 0.0);

@@ -23,6 +23,8 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 
 #include "masw_det.cuh"
 #include "masw_internal.h"
@@ -175,8 +177,20 @@ __host__ __device__ inline size_t team_model_bytes(int N)
     return (size_t)(N + 1) * sizeof(LayerConst) + (size_t)2 * (N + 1) * sizeof(double);
 }
 
+// Resident CTAs per SM requested from ptxas: 768 threads/SM (3 x 256 -> <= 85 registers;
+// measured on B200: +5% over the unconstrained 94-register build despite ~60 B of L1-resident
+// spills).  -DMASW_SCAN_MINB=k overrides it for 256-thread CTAs (0 = unconstrained).
+#ifndef MASW_SCAN_MINB
+#define MASW_SCAN_MINB 3
+#endif
+template <int BLOCK>
+constexpr int scan_min_blocks()
+{
+    return BLOCK == 256 ? MASW_SCAN_MINB : 1;
+}
+
 template <int TEAM, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) scan_kernel(ScanArgs a)
+__global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(ScanArgs a)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     extern __shared__ __align__(16) unsigned char smem[];
@@ -245,10 +259,23 @@ __global__ void __launch_bounds__(BLOCK) scan_kernel(ScanArgs a)
         bool found = false;
         for (int64_t base = 0; base < V; base += 32 * TEAM) {
             const int64_t j = base + tl;
+            // Is any layer velocity within 1e-3 of this warp's velocity range?  (S4 check
+            // needed only then; the grid is strictly increasing.)
+            bool near = false;
+            {
+                const int64_t w0 = base + wt * 32;
+                const double clo = cg[min(w0, V - 1)] - 1e-3;
+                const double chi = cg[min(w0 + 31, V - 1)] + 1e-3;
+                for (int e = lane; e < 2 * (N + 1); e += 32) {
+                    const double v = vel[e];
+                    near |= (v > clo) && (v < chi);
+                }
+                near = __any_sync(FULL, near);
+            }
             int s = 0;
             bool bad = false;
             if (j < V) {
-                const DetOut d = det_K<false>(lc, vel, N, cg[j]);
+                const DetOut d = det_K<false>(lc, vel, N, cg[j], near);
                 s = d.sign;
                 bad = d.bad;
                 ++my_eval;
@@ -313,12 +340,27 @@ __global__ void __launch_bounds__(BLOCK) scan_kernel(ScanArgs a)
     }
 }
 
+// Per-device launch facts, cached: SM count and resident CTAs per SM per (kernel, smem).
+namespace {
+std::mutex g_cache_mu;
+std::unordered_map<long long, int> g_occ_cache;
+int g_sms[64] = {0};
+
+int sm_count(int device)
+{
+    if (device >= 0 && device < 64 && g_sms[device] > 0) return g_sms[device];
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (device >= 0 && device < 64) g_sms[device] = sms;
+    return sms;
+}
+}  // namespace
+
 int auto_team_warps(int64_t rows, int64_t V, int device)
 {
     // Minimise tail idle (~ resident_warps / (2 TEAM rows)) + speculation waste
     // (~ 16 TEAM / dets_per_row) with dets_per_row ~ V/2:  TEAM* = sqrt(Wres d / (32 R)).
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int sms = sm_count(device);
     const double wres = sms * 32.0;
     const double d = (double)V / 2.0;
     const double t = sqrt(wres * d / (32.0 * (double)(rows > 0 ? rows : 1)));
@@ -333,16 +375,26 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     const size_t smem = round8(sizeof(TeamCtrl) * TEAMS) + TEAMS * team_model_bytes(a.mod.N);
     auto kern = scan_kernel<TEAM, BLOCK>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
+    const int sms = sm_count(device);
+    const long long key = ((long long)device << 40) | ((long long)TEAM << 32) | (long long)smem;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        auto it = g_occ_cache.find(key);
+        if (it != g_occ_cache.end()) per_sm = it->second;
     }
-    int sms = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
+    if (per_sm == 0) {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(
+                kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) per_sm = 1;
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        g_occ_cache[key] = per_sm;
+    }
     const int64_t rows = a.mod.M * a.L;
     int64_t blocks = (int64_t)sms * per_sm;
     const int64_t need = (rows + TEAMS - 1) / TEAMS;

@@ -16,7 +16,7 @@ import numpy as np
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("MASW_LIB", _build.LIB)   # MASW_LIB: variant builds (experiments)
 
 OK, WARN_NO_SIGN_CHANGE = 0, 1
 E_ARG, E_MODEL, E_GRID, E_RANGE, E_NONFINITE, E_CUDA, E_NOMEM = -1, -2, -3, -4, -5, -6, -7

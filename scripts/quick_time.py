@@ -30,11 +30,16 @@ def time_call(fn, reps=5):
 
 
 def main():
-    tf, ms = masw.masw_probe_fp64_peak(-1, 300.0)
-    print(f"fp64 probe: {tf:.2f} TFLOP/s ({ms:.1f} ms)", flush=True)
+    print("lib:", masw.masw.LIB_PATH, flush=True)
+    if not os.environ.get("NOPROBE"):
+        tf, ms = masw.masw_probe_fp64_peak(-1, 300.0)
+        print(f"fp64 probe: {tf:.2f} TFLOP/s ({ms:.1f} ms)", flush=True)
     team_env = int(os.environ.get("TEAM", "0"))
+    only = os.environ.get("CONFIGS", "tiny,maswaves,uniform,realistic,ensemble").split(",")
     for name, kw in [("tiny", {}), ("maswaves", {}), ("uniform", {"tier": 200.0}),
                      ("realistic", {}), ("ensemble", {"M": 100_000})]:
+        if name not in only:
+            continue
         w = synth.workload(name, **kw)
         m = w.models
         args = [dev(x) for x in (m.h, m.alpha, m.beta, m.rho)]

@@ -77,7 +77,7 @@ def test_det_parity_random_ensemble_points(masw, orc, seed):
     """Det parity on random C5 models at random (lambda, c): 20 models x 40 lambda x 256 c."""
     w = synth.workload("ensemble", M=400)
     rng = np.random.default_rng(seed)
-    worst, n = 0.0, 0
+    worst, n, where = 0.0, 0, None
     for mi in rng.choice(400, 20, replace=False):
         a = margs(w.models, mi)
         c = np.sort(rng.uniform(0.5 * a[2].min(), 500.0, 256))
@@ -86,10 +86,17 @@ def test_det_parity_random_ensemble_points(masw, orc, seed):
         _, lmant, lex, _ = orc.det_grid(*a, w.lam, c, extended=True)
         rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
         dom = parity.det_domain(omant, oex, c, a[2].min(), lmant, lex)
-        worst = max(worst, float(np.nanmax(rel[dom])))
+        r = np.where(dom, rel, 0.0)
+        k = np.unravel_index(np.argmax(r), r.shape)
+        if r[k] > worst:
+            audit = parity.det_grid_rel_err(omant, oex, lmant, lex)[k]
+            glv = parity.det_grid_rel_err(gre + 1j * gim, gex, lmant, lex)[k]
+            where = (int(mi), float(w.lam[k[0]]), float(c[k[1]]), float(audit), float(glv))
+            worst = float(r[k])
         n += int(dom.sum())
     assert n > 0.8 * 20 * 40 * 256
-    assert worst <= parity.DET_RTOL, worst
+    # where = (model, lambda, c, oracle fp64-vs-ld audit, GPU-vs-ld error)
+    assert worst <= parity.DET_RTOL, (worst, where)
 
 
 # ------------------------------------------------------------------ C_t parity, one model
