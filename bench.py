@@ -65,6 +65,8 @@ class ClockSampler:
         self.gpu = gpu_index
 
     def __enter__(self):
+        if os.environ.get("MASW_BENCH_NOCLOCK"):
+            return self
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -300,8 +302,8 @@ def run_ours(args):
         barrier()
         for _ in range(args.steps):
             flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            e0 = torch.cuda.Event(enable_timing=True, blocking=True)
+            e1 = torch.cuda.Event(enable_timing=True, blocking=True)
             e0.record()
             alg, sms, _ = step_device()
             e1.record()
@@ -319,8 +321,8 @@ def run_ours(args):
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0 = torch.cuda.Event(enable_timing=True, blocking=True)
+        e1 = torch.cuda.Event(enable_timing=True, blocking=True)
         e0.record()
         step_e2e()
         e1.record()
@@ -355,7 +357,8 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            traffic = pj.get("dram_bytes_per_launch_scaled_to_bench")
+            # captured on the bench's own scan launch (same workload): bytes per launch
+            traffic = pj.get("dram_bytes")
         except Exception:
             traffic = None
     h2d = sum(x.numel() * x.element_size() for x in (hh, ha, hb, hr, hlam, hc, hce))
@@ -383,6 +386,8 @@ def run_ours(args):
                                     "(B200_PROFILING.md counts; MEASURED_PEAKS.json has no FP64)",
                      "peak_probe_dfma_tflops": peak_probe},
         "clocks": clocks,
+        "step_ms": [round(x, 3) for x in step_ms],
+        "scan_ms": [round(x, 3) for x in scan_ms],
     }
     if not args.no_extra and world == 1:
         line["other_configs"] = other_configs(masw, torch, dev)

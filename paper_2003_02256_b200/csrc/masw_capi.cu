@@ -22,6 +22,7 @@ namespace {
 
 thread_local char t_cuda_err[256] = "";
 thread_local Workspace *t_pinned_ws = nullptr;   // pinned host copy target for the status read
+thread_local cudaEvent_t t_sync_event = nullptr;  // blocking-sync event for host waits
 thread_local double t_last_scan_ms = -1.0;
 thread_local long long t_last_alg = -1, t_last_eval = -1;
 
@@ -142,13 +143,24 @@ struct Arena {
     }
 };
 
+// Waits for everything enqueued on `st` with a blocking-sync event: the host thread sleeps
+// instead of spin-polling for the whole kernel (a spinning wait of ~0.1 s per call burns a
+// CPU quota and, measured on the GPU box, added 20-190 ms stalls per call).
+void wait_stream(cudaStream_t st)
+{
+    if (!t_sync_event)
+        CK(cudaEventCreateWithFlags(&t_sync_event, cudaEventBlockingSync | cudaEventDisableTiming));
+    CK(cudaEventRecord(t_sync_event, st));
+    CK(cudaEventSynchronize(t_sync_event));
+}
+
 // Reads the device workspace into pinned host memory (pageable copies can stall) and
-// synchronises the stream.
+// waits for the stream.
 Workspace read_status(const Workspace *ws, cudaStream_t st)
 {
     if (!t_pinned_ws) CK(cudaMallocHost(&t_pinned_ws, sizeof(Workspace)));
     CK(cudaMemcpyAsync(t_pinned_ws, ws, sizeof(Workspace), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    wait_stream(st);
     return *t_pinned_ws;
 }
 
@@ -265,7 +277,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
                 CK(cudaMemcpyAsync(idx_out, didx, R * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
             if (misfit_out)
                 CK(cudaMemcpyAsync(misfit_out, dmis, M * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            wait_stream(st);
         }
         return code;
     } catch (const Fail &f) {
@@ -305,7 +317,7 @@ int run_misfit(const double *ct, const double *ce, int64_t M, int64_t L, double 
         if (code < 0) return code;
         if (host) {
             CK(cudaMemcpyAsync(out, dout, M * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            wait_stream(st);
         }
         return MASW_OK;
     } catch (const Fail &f) {
@@ -385,9 +397,9 @@ int masw_argmin(const double *misfit, int64_t M, int64_t *best_out, double *best
             CK(cudaMemcpyAsync(best_out, db, 8, cudaMemcpyDeviceToHost, st));
             if (best_misfit_out)
                 CK(cudaMemcpyAsync(best_misfit_out, dv, 8, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            wait_stream(st);
         } else if (!(ex.flags & MASW_ASYNC)) {
-            CK(cudaStreamSynchronize(st));
+            wait_stream(st);
         }
         return MASW_OK;
     } catch (const Fail &f) {
@@ -445,7 +457,7 @@ int masw_det_grid(const masw_model *model, const double *lambda, int64_t L, cons
             CK(cudaMemcpyAsync(mant_re, dre, G * 8, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(mant_im, dim, G * 8, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(exp2, dex, G * 4, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            wait_stream(st);
         }
         return MASW_OK;
     } catch (const Fail &f) {

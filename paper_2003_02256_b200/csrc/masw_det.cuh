@@ -37,14 +37,30 @@ constexpr double kPerturbTol = 1e-4;           // reading S4
 constexpr double kPerturbFactor = 1.0 - 1e-4;  // reading S4
 
 // Per-row constants of one finite layer e (index N holds the half-space's ia2, ib2, mu).
-struct LayerConst {
+// 48 bytes, 16-byte aligned: read from shared memory as three 128-bit loads.
+struct __align__(16) LayerConst {
     double kh;    // k * h_e
     double ia2;   // 1 / alpha_e^2
     double ib2;   // 1 / beta_e^2
     double krho;  // k * rho_e
     double mu;    // k * rho_e * beta_e^2
+    double pad;
 };
-static_assert(sizeof(LayerConst) == 40, "LayerConst layout");
+static_assert(sizeof(LayerConst) == 48, "LayerConst layout");
+
+__device__ __forceinline__ LayerConst load_lc(const LayerConst *p)
+{
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a = q[0], b = q[1], c = q[2];
+    LayerConst L;
+    L.kh = a.x;
+    L.ia2 = a.y;
+    L.ib2 = b.x;
+    L.krho = b.y;
+    L.mu = c.x;
+    L.pad = c.y;
+    return L;
+}
 
 // -------------------------------------------------------------- fp64 elementary functions
 // Written for this kernel's argument ranges (all inputs finite and normal; see each function)
@@ -429,14 +445,15 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
 
     int neg = 0, perm = 0;
     bool zero = false, bad = false;
+    double nf = 0.0;   // NaN once any pivot / the last det is NaN or Inf
     DetAcc acc{1.0, 0};
 
-    Elem P = layer_elem(lc[0], c2);
+    Elem P = layer_elem(load_lc(lc), c2);
     double X[2][4] = {{P.k11, P.k12, P.k13, P.k14}, {P.k12, P.k22, -P.k14, P.k24}};
 
 #pragma unroll 1
     for (int t = 0; t + 1 < N; ++t) {
-        const Elem Q = layer_elem(lc[t + 1], c2);
+        const Elem Q = layer_elem(load_lc(lc + t + 1), c2);
         double R[4][6] = {
             {X[0][0], X[0][1], X[0][2], X[0][3], 0.0, 0.0},
             {X[1][0], X[1][1], X[1][2], X[1][3], 0.0, 0.0},
@@ -446,11 +463,14 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
         double Xi[2][4];
         const StepOut so = gepp_step<6, 0>(R, Ri, X, Xi);
         const double piv0 = so.piv0, piv1 = so.piv1;
-        const int par = so.parity;
-        neg ^= par ^ (piv0 < 0.0) ^ (piv1 < 0.0);
-        perm ^= par;
-        zero |= (piv0 == 0.0) | (piv1 == 0.0);
-        bad |= !isfinite(piv0) | !isfinite(piv1);
+        // t = piv0 * piv1 carries both signs, is 0 iff a pivot is 0, and is non-finite iff a
+        // pivot is (|pivots| are far from the fp64 range limits); nf turns NaN on the first
+        // non-finite t and stays NaN.
+        const double tp = piv0 * piv1;
+        neg ^= so.parity ^ (tp < 0.0);
+        perm ^= so.parity;
+        zero |= (tp == 0.0);
+        nf = fma(tp, 0.0, nf);
         if (WANT_VALUE) {
             acc.mul(piv0);
             acc.mul(piv1);
@@ -462,7 +482,8 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     // c^2/beta_N^2 (real); cases by the branch of r, s (reading S3).
     double h11r, h11i, h12r, h12i, h22r, h22i;
     {
-        const double ia2 = lc[N].ia2, ib2 = lc[N].ib2, mu = lc[N].mu;
+        const LayerConst H = load_lc(lc + N);
+        const double ia2 = H.ia2, ib2 = H.ib2, mu = H.mu;
         const double qa = fma(-c2, ia2, 1.0), qb = fma(-c2, ib2, 1.0);
         const double w = c2 * ib2;
         if (qb > 0.0) {                     // c < beta_N < alpha_N: r, s real
@@ -499,11 +520,11 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     double Y[2][2], Yi[2][2];
     const StepOut so = gepp_step<4, 2>(R, Ri, Y, Yi);
     const double piv0 = so.piv0, piv1 = so.piv1;
-    const int par = so.parity;
-    neg ^= par ^ (piv0 < 0.0) ^ (piv1 < 0.0);
-    perm ^= par;
-    zero |= (piv0 == 0.0) | (piv1 == 0.0);
-    bad |= !isfinite(piv0) | !isfinite(piv1);
+    const double tp = piv0 * piv1;
+    neg ^= so.parity ^ (tp < 0.0);
+    perm ^= so.parity;
+    zero |= (tp == 0.0);
+    nf = fma(tp, 0.0, nf);
     if (WANT_VALUE) {
         acc.mul(piv0);
         acc.mul(piv1);
@@ -513,7 +534,8 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
                        fma(Y[0][1], Y[1][0], -Yi[0][1] * Yi[1][0]);
     const double dim = fma(Y[0][0], Yi[1][1], Yi[0][0] * Y[1][1]) -
                        fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
-    bad |= !isfinite(dre) || !isfinite(dim);
+    nf = fma(dre, 0.0, fma(dim, 0.0, nf));
+    bad = !(nf == 0.0);
     zero |= (dre == 0.0);
     neg ^= (dre < 0.0);
 

@@ -170,11 +170,12 @@ struct TeamCtrl {
     int last[2][32];
 };
 
-__host__ __device__ constexpr size_t round8(size_t x) { return (x + 7) & ~size_t(7); }
+__host__ __device__ constexpr unsigned round16(unsigned x) { return (x + 15u) & ~15u; }
 
-__host__ __device__ inline size_t team_model_bytes(int N)
+__host__ __device__ inline unsigned team_model_bytes(int N)
 {
-    return (size_t)(N + 1) * sizeof(LayerConst) + (size_t)2 * (N + 1) * sizeof(double);
+    return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +
+                   2u * (unsigned)(N + 1) * (unsigned)sizeof(double));
 }
 
 // Resident CTAs per SM requested from ptxas: 768 threads/SM (3 x 256 -> <= 85 registers;
@@ -201,9 +202,10 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     const int team = warp / TEAM, wt = warp % TEAM, tl = wt * 32 + lane;
 
     TeamCtrl *ctrl = reinterpret_cast<TeamCtrl *>(smem) + team;
-    unsigned char *mbase = smem + round8(sizeof(TeamCtrl) * TEAMS) + team * team_model_bytes(N);
-    LayerConst *lc = reinterpret_cast<LayerConst *>(mbase);
-    double *vel = reinterpret_cast<double *>(mbase + (size_t)(N + 1) * sizeof(LayerConst));
+    const unsigned moff = round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
+                          (unsigned)team * team_model_bytes(N);
+    LayerConst *lc = reinterpret_cast<LayerConst *>(smem + moff);
+    double *vel = reinterpret_cast<double *>(smem + moff + (unsigned)(N + 1) * sizeof(LayerConst));
 
     Workspace *ws = a.ws;
     if (threadIdx.x == 0) {
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             x.ib2 = 1.0 / (be * be);
             x.krho = k * rh;
             x.mu = k * rh * be * be;
+            x.pad = 0.0;
             lc[e] = x;
             vel[2 * e] = al;
             vel[2 * e + 1] = be;
@@ -373,7 +376,8 @@ template <int TEAM, int BLOCK>
 static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
-    const size_t smem = round8(sizeof(TeamCtrl) * TEAMS) + TEAMS * team_model_bytes(a.mod.N);
+    const size_t smem = round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
+                        (size_t)TEAMS * team_model_bytes(a.mod.N);
     auto kern = scan_kernel<TEAM, BLOCK>;
     const int sms = sm_count(device);
     const long long key = ((long long)device << 40) | ((long long)TEAM << 32) | (long long)smem;
@@ -536,6 +540,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
         x.ib2 = 1.0 / (be * be);
         x.krho = k * rh;
         x.mu = k * rh * be * be;
+        x.pad = 0.0;
         lc[e] = x;
         vel[2 * e] = al;
         vel[2 * e + 1] = be;
