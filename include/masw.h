@@ -156,8 +156,14 @@ const char *masw_last_cuda_error(void);
 int64_t masw_kernel_launches(void);
 
 /* Device time in ms of the calling thread's last scan kernel launched with MASW_TIME_SCAN
- * (CUDA events on the launching stream); -1 if none. */
+ * (CUDA events recorded around the launch on the launching stream; for a MASW_ASYNC call the
+ * first query waits for the end event); -1 if none. */
 double masw_last_scan_ms(void);
+
+/* Device times in ms of the calling thread's most recent MASW_TIME_SCAN scan launches (up to
+ * the last 64), oldest first, into ms_out[0..n); waits for their end events.  Returns the
+ * number written (<= n) or MASW_E_ARG. */
+int masw_recent_scan_ms(double *ms_out, int32_t n);
 
 /* Algorithmic work of the calling thread's last curve/ensemble call: the early-exit
  * determinant count sum_rows (idx+1) of SPEC.md:246 (rows with idx < 0 count V for -1 and

@@ -22,8 +22,11 @@ namespace {
 
 thread_local char t_cuda_err[256] = "";
 thread_local Workspace *t_pinned_ws = nullptr;   // pinned host copy target for the status read
-thread_local cudaEvent_t t_sync_event = nullptr;  // blocking-sync event for host waits
-thread_local double t_last_scan_ms = -1.0;
+// Scan-kernel timing events of the calling thread (MASW_TIME_SCAN): a ring of the last
+// kScanRing launches, resolved lazily so MASW_ASYNC calls can be timed without host waits.
+constexpr int kScanRing = 64;
+thread_local cudaEvent_t t_scan_ev[kScanRing][2] = {};
+thread_local long long t_scan_count = 0;   // TIME_SCAN launches recorded by this thread
 thread_local long long t_last_alg = -1, t_last_eval = -1;
 
 struct Fail {
@@ -143,15 +146,11 @@ struct Arena {
     }
 };
 
-// Waits for everything enqueued on `st` with a blocking-sync event: the host thread sleeps
-// instead of spin-polling for the whole kernel (a spinning wait of ~0.1 s per call burns a
-// CPU quota and, measured on the GPU box, added 20-190 ms stalls per call).
+// Waits for everything enqueued on `st` (spin-wait: a blocking-sync event was measured to
+// wake up 10-700 ms late on the GPU box; callers that must not wait use MASW_ASYNC).
 void wait_stream(cudaStream_t st)
 {
-    if (!t_sync_event)
-        CK(cudaEventCreateWithFlags(&t_sync_event, cudaEventBlockingSync | cudaEventDisableTiming));
-    CK(cudaEventRecord(t_sync_event, st));
-    CK(cudaEventSynchronize(t_sync_event));
+    CK(cudaStreamSynchronize(st));
 }
 
 // Reads the device workspace into pinned host memory (pageable copies can stall) and
@@ -241,32 +240,22 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
 
         const int team = ex.team ? ex.team : auto_team_warps(R, V, dev);
         ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws, dce ? 0x7Fu : 0x1Fu};
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
         const bool timed = (ex.flags & MASW_TIME_SCAN) != 0;
+        cudaEvent_t *slot = t_scan_ev[t_scan_count % kScanRing];
         if (timed) {
-            CK(cudaEventCreate(&e0));
-            CK(cudaEventCreate(&e1));
-            CK(cudaEventRecord(e0, st));
+            if (!slot[0]) CK(cudaEventCreate(&slot[0]));
+            if (!slot[1]) CK(cudaEventCreate(&slot[1]));
+            CK(cudaEventRecord(slot[0], st));
         }
         CK(launch_scan(sa, team, st, dev));
-        if (timed) CK(cudaEventRecord(e1, st));
+        if (timed) {
+            CK(cudaEventRecord(slot[1], st));
+            ++t_scan_count;
+        }
         if (dmis) CK(launch_misfit(dct, dce, M, L, dmis, ws, 0x7Fu, true, st));
 
-        if (!host && (ex.flags & MASW_ASYNC)) {
-            if (timed) {
-                cudaEventDestroy(e0);
-                cudaEventDestroy(e1);
-            }
-            return MASW_OK;
-        }
+        if (!host && (ex.flags & MASW_ASYNC)) return MASW_OK;
         const Workspace w = read_status(ws, st);
-        if (timed) {
-            float ms = -1.0f;
-            CK(cudaEventElapsedTime(&ms, e0, e1));
-            t_last_scan_ms = ms;
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-        }
         const int code = decode(w, dce != nullptr, true);
         if (code < 0) return code;
         t_last_alg = (long long)w.alg_dets;
@@ -487,7 +476,30 @@ const char *masw_last_cuda_error(void) { return t_cuda_err; }
 
 int64_t masw_kernel_launches(void) { return (int64_t)launches(); }
 
-double masw_last_scan_ms(void) { return t_last_scan_ms; }
+int masw_recent_scan_ms(double *ms_out, int32_t n)
+{
+    if (!ms_out || n < 0) return MASW_E_ARG;
+    long long avail = t_scan_count < kScanRing ? t_scan_count : kScanRing;
+    if (n > avail) n = (int32_t)avail;
+    for (int32_t i = 0; i < n; ++i) {
+        const long long k = t_scan_count - n + i;   // oldest first
+        cudaEvent_t *slot = t_scan_ev[k % kScanRing];
+        float ms = -1.0f;
+        if (cudaEventSynchronize(slot[1]) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, slot[0], slot[1]) != cudaSuccess) {
+            cudaGetLastError();
+            ms = -1.0f;
+        }
+        ms_out[i] = ms;
+    }
+    return n;
+}
+
+double masw_last_scan_ms(void)
+{
+    double ms = -1.0;
+    return masw_recent_scan_ms(&ms, 1) == 1 ? ms : -1.0;
+}
 
 int masw_last_work(int64_t *algorithmic_dets, int64_t *evaluated_dets)
 {

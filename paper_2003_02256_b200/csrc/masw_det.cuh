@@ -125,75 +125,48 @@ __device__ __forceinline__ double scale2(double x, int k)
     return __hiloint2double(__double2hiint(x) + (k << 20), __double2loint(x));
 }
 
-// cosh and sinh of th in [0, 700]; the caller guarantees th <= 350 (range guard S9).
-// Below 1 the Taylor series (no cancellation in sinh); above, exp and 1/exp, where
-// sinh = A - B loses at most a factor coth(1) = 1.31.
+// cosh and sinh of th in [0, 700] without branches (the caller guarantees th <= 350, range
+// guard S9).  th = n ln2 + r, |r| <= ln2/2, em1 = e^r - 1 by its Taylor series to r^14
+// (no constant term, so it is accurate for tiny r), p = 1 + em1, q = 1/p, and with
+// a = 2^(n-1), b = 2^(-n-1):
+//   cosh = a p + b q
+//   sinh = (a - b) + a em1 + b em1 q        (e^r - e^-r = em1 + em1/p: no cancellation at n=0)
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
 {
-    if (th < 1.0) {
-        // sinh(t)/t = sum t^{2n}/(2n+1)!, n <= 9 (truncation < 1e-17 for t < 1);
-        // cosh(t) = sum t^{2n}/(2n)!, n <= 10 (truncation < 5e-19).
-        const double t2 = th * th;
-        double ps = c_invfact[19];
-        ps = fma(ps, t2, c_invfact[17]);
-        ps = fma(ps, t2, c_invfact[15]);
-        ps = fma(ps, t2, c_invfact[13]);
-        ps = fma(ps, t2, c_invfact[11]);
-        ps = fma(ps, t2, c_invfact[9]);
-        ps = fma(ps, t2, c_invfact[7]);
-        ps = fma(ps, t2, c_invfact[5]);
-        ps = fma(ps, t2, c_invfact[3]);
-        ps = fma(ps, t2, 1.0);
-        double pc = c_invfact[20];
-        pc = fma(pc, t2, c_invfact[18]);
-        pc = fma(pc, t2, c_invfact[16]);
-        pc = fma(pc, t2, c_invfact[14]);
-        pc = fma(pc, t2, c_invfact[12]);
-        pc = fma(pc, t2, c_invfact[10]);
-        pc = fma(pc, t2, c_invfact[8]);
-        pc = fma(pc, t2, c_invfact[6]);
-        pc = fma(pc, t2, c_invfact[4]);
-        pc = fma(pc, t2, 0.5);
-        pc = fma(pc, t2, 1.0);
-        sh = th * ps;
-        ch = pc;
-    } else {
-        // th = n ln2 + r, |r| <= ln2/2; e^r by its Taylor series to r^13 (< 5e-18);
-        // e^-r = 1/e^r with e^r in [0.7, 1.42]; cosh, sinh = 2^(n-1) e^r +- 2^(-n-1) e^-r.
-        const double t = fma(th, kLog2e, kShifter);
-        const double nd = t - kShifter;
-        const int n = __double2loint(t);
-        double r = fma(nd, -kLn2Hi, th);
-        r = fma(nd, -kLn2Lo, r);
-        double p = c_invfact[13];
-        p = fma(p, r, c_invfact[12]);
-        p = fma(p, r, c_invfact[11]);
-        p = fma(p, r, c_invfact[10]);
-        p = fma(p, r, c_invfact[9]);
-        p = fma(p, r, c_invfact[8]);
-        p = fma(p, r, c_invfact[7]);
-        p = fma(p, r, c_invfact[6]);
-        p = fma(p, r, c_invfact[5]);
-        p = fma(p, r, c_invfact[4]);
-        p = fma(p, r, c_invfact[3]);
-        p = fma(p, r, 0.5);
-        p = fma(p, r, 1.0);
-        p = fma(p, r, 1.0);
-        const double q = rcp_fast(p);
-        const double A = scale2(p, n - 1), B = scale2(q, -n - 1);
-        ch = A + B;
-        sh = A - B;
-    }
+    const double t = fma(th, kLog2e, kShifter);
+    const double nd = t - kShifter;
+    const int n = __double2loint(t);
+    double r = fma(nd, -kLn2Hi, th);
+    r = fma(nd, -kLn2Lo, r);
+    double e = c_invfact[14];
+    e = fma(e, r, c_invfact[13]);
+    e = fma(e, r, c_invfact[12]);
+    e = fma(e, r, c_invfact[11]);
+    e = fma(e, r, c_invfact[10]);
+    e = fma(e, r, c_invfact[9]);
+    e = fma(e, r, c_invfact[8]);
+    e = fma(e, r, c_invfact[7]);
+    e = fma(e, r, c_invfact[6]);
+    e = fma(e, r, c_invfact[5]);
+    e = fma(e, r, c_invfact[4]);
+    e = fma(e, r, c_invfact[3]);
+    e = fma(e, r, 0.5);
+    e = fma(e, r, 1.0);
+    const double em1 = e * r;
+    const double p = 1.0 + em1;
+    const double q = rcp_fast(p);
+    const double a = __hiloint2double((n + 1022) << 20, 0);    // 2^(n-1)
+    const double b = __hiloint2double((1022 - n) << 20, 0);    // 2^(-n-1)
+    ch = fma(a, p, b * q);
+    sh = fma(a, em1, fma(b * em1, q, a - b));
 }
 
-// sin and cos of th in [0, 2^19 * pi/2) (Cody-Waite reduction, Taylor on |r| <= pi/4:
-// sin to r^15, cos to r^16, truncation < 1e-16).  Larger arguments use libm.
+// sin and cos of th in [0, 8e5] (< 2^19 pi/2: Cody-Waite reduction exact; Taylor on
+// |r| <= pi/4: sin to r^15, cos to r^16, truncation < 1e-16).  No branches; the caller
+// routes larger arguments to libm.
+constexpr double kTrigMax = 8.0e5;
 __device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
 {
-    if (th >= 8.0e5) {
-        sincos(th, &sn, &cs);
-        return;
-    }
     const double t = fma(th, kTwoOverPi, kShifter);
     const double nd = t - kShifter;
     const int n = __double2loint(t);
@@ -228,27 +201,42 @@ __device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
     cs = __hiloint2double((int)((unsigned)__double2hiint(b) ^ sgn_c), __double2loint(b));
 }
 
-// -------------------------------------------------------------- wave triple
-// (C, XS, SX) for q = 1 - c^2/v^2 != 0 and kh = k*h.  See header comment.
+// -------------------------------------------------------------- wave triples
+// (C, XS, SX) of one wave: q = 1 - c^2/v^2 (!= 0 by S4) and kh = k*h; see header comment.
+__device__ __forceinline__ void wave_hyp(double q, double kh, double &C, double &XS, double &SX)
+{
+    double x, rq;                      // x, 1/x
+    sqrt_rsqrt(q, x, rq);
+    double ch, sh;
+    cosh_sinh(kh * x, ch, sh);
+    C = ch;
+    XS = x * sh;
+    SX = sh * rq;
+}
+
+__device__ __forceinline__ void wave_trig(double q, double kh, double &C, double &XS, double &SX)
+{
+    double xi, rq;                     // xi, 1/xi
+    sqrt_rsqrt(-q, xi, rq);
+    const double th = kh * xi;
+    double sn, cs;
+    if (th < kTrigMax) {
+        sin_cos(th, sn, cs);
+    } else {
+        sincos(th, &sn, &cs);
+    }
+    C = cs;
+    XS = -xi * sn;
+    SX = sn * rq;
+}
+
 __device__ __forceinline__ void wave_triple(double q, double kh, double &C, double &XS,
                                             double &SX)
 {
     if (q > 0.0) {
-        double x, rq;                      // x, 1/x
-        sqrt_rsqrt(q, x, rq);
-        double ch, sh;
-        cosh_sinh(kh * x, ch, sh);
-        C = ch;
-        XS = x * sh;
-        SX = sh * rq;
+        wave_hyp(q, kh, C, XS, SX);
     } else {
-        double xi, rq;                     // xi, 1/xi
-        sqrt_rsqrt(-q, xi, rq);
-        double sn, cs;
-        sin_cos(kh * xi, sn, cs);
-        C = cs;
-        XS = -xi * sn;
-        SX = sn * rq;
+        wave_trig(q, kh, C, XS, SX);
     }
 }
 
@@ -283,8 +271,20 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
     const double qb = fma(-c2, L.ib2, 1.0);   // s^2
     double Cr, XSr, SXr, Cs, XSs, SXs;
-    wave_triple(qa, L.kh, Cr, XSr, SXr);
-    wave_triple(qb, L.kh, Cs, XSs, SXs);
+    // The P wave is hyperbolic unless c exceeds alpha (rare); each S-wave branch carries its
+    // own branch-free copy of the P wave so the two independent chains interleave (ILP).
+    if (qa > 0.0) {
+        if (qb > 0.0) {
+            wave_hyp(qa, L.kh, Cr, XSr, SXr);
+            wave_hyp(qb, L.kh, Cs, XSs, SXs);
+        } else {
+            wave_hyp(qa, L.kh, Cr, XSr, SXr);
+            wave_trig(qb, L.kh, Cs, XSs, SXs);
+        }
+    } else {
+        wave_triple(qa, L.kh, Cr, XSr, SXr);
+        wave_triple(qb, L.kh, Cs, XSs, SXs);
+    }
     const double CC = Cr * Cs;
     const double D = fma(SXr, SXs, fma(XSr, XSs, 2.0 * (1.0 - CC)));
     const double f = (L.krho * c2) * rcp_fast(D);

@@ -77,6 +77,7 @@ def lib():
         L.masw_last_cuda_error.restype = ctypes.c_char_p
         L.masw_kernel_launches.restype = ctypes.c_int64
         L.masw_last_scan_ms.restype = ctypes.c_double
+        L.masw_recent_scan_ms.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int32]
         L.masw_last_work.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
         L.masw_probe_fp64_peak.argtypes = [ctypes.c_int32, ctypes.c_double,
                                            ctypes.POINTER(ctypes.c_double),
@@ -230,13 +231,13 @@ def masw_misfit_batch(ct, ce, *, stream=None, misfit_out=None):
     return bo.obj
 
 
-def masw_argmin(misfit, *, stream=None):
+def masw_argmin(misfit, *, stream=None, flags=0):
     """(best index, best misfit), ties → lowest index."""
     bm = _Buf(misfit, np.float64)
-    b = _empty_like_kind(bm, (1,), np.int64, fill=-1)
-    v = _empty_like_kind(bm, (1,), np.float64, fill=np.nan)
+    b = _empty_like_kind(bm, (1,), np.int64)
+    v = _empty_like_kind(bm, (1,), np.float64)
     bb, bv = _Buf(b, np.int64), _Buf(v, np.float64)
-    ex = _exec(bm, 0, 0, stream)
+    ex = _exec(bm, 0, flags, stream)
     _check(lib().masw_argmin(bm.ptr, len(bm.obj), bb.ptr, bv.ptr, ctypes.byref(ex)),
            "masw_argmin")
     return bb.obj, bv.obj
@@ -263,6 +264,13 @@ def masw_kernel_launches() -> int:
 
 def masw_last_scan_ms() -> float:
     return float(lib().masw_last_scan_ms())
+
+
+def masw_recent_scan_ms(n: int):
+    """Scan-kernel device times (ms) of the last n MASW_TIME_SCAN launches, oldest first."""
+    buf = (ctypes.c_double * max(n, 1))()
+    k = lib().masw_recent_scan_ms(buf, n)
+    return [buf[i] for i in range(max(k, 0))]
 
 
 def masw_last_work():
