@@ -364,13 +364,17 @@ def run_ours(args):
     kern_ms = statistics.mean(scan_ms)
     achieved = my_dets_per_step * F / (kern_ms / 1e3) / 1e12
     peak = fp64_peak_tflops()
-    traffic = None
+    traffic, hw = None, {}
     prof = os.path.join(ROOT, "profiles", "scan_kernel_ncu.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
             # captured on the bench's own scan launch (same workload): bytes per launch
             traffic = pj.get("dram_bytes")
+            hw = {"fp64_pipe_pct_active": pj.get("fp64_pipe_pct_active"),
+                  "hw_fp64_tflops": pj.get("hw_fp64_tflops"),
+                  "hw_fp64_frac_of_derived_peak": pj.get("hw_fp64_frac_of_derived_peak"),
+                  "source": "profiles/scan_kernel_ncu.json (ncu --set full of this launch)"}
         except Exception:
             traffic = None
     h2d = sum(x.numel() * x.element_size() for x in (hh, ha, hb, hr, hlam, hc, hce))
@@ -396,7 +400,8 @@ def run_ours(args):
                      "kernel_ms": kern_ms, "flops_per_det": F,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
                                     "(B200_PROFILING.md counts; MEASURED_PEAKS.json has no FP64)",
-                     "peak_probe_dfma_tflops": peak_probe},
+                     "peak_probe_dfma_tflops": peak_probe,
+                     "hardware_fp64": hw},
         "clocks": clocks,
         "step_ms": [round(x, 3) for x in step_ms],
         "scan_ms": [round(x, 3) for x in scan_ms],

@@ -163,8 +163,18 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
 
 // sin and cos of th in [0, 8e5] (< 2^19 pi/2: Cody-Waite reduction exact; Taylor on
 // |r| <= pi/4: sin to r^15, cos to r^16, truncation < 1e-16).  No branches; the caller
-// routes larger arguments to libm.
+// routes larger arguments to sin_cos_large.
 constexpr double kTrigMax = 8.0e5;
+// pi/2 in five parts, the first four of <= 23 significant bits: n * part is exact for
+// n < 2^30, so the large-argument reduction below is accurate for th < 2^30 * pi/2.
+constexpr double kPio2L_1 = 1.570796251296997;
+constexpr double kPio2L_2 = 7.549789415861596e-08;
+constexpr double kPio2L_3 = 5.390302529957765e-15;
+constexpr double kPio2L_4 = 3.2820036682434026e-22;
+constexpr double kPio2L_5 = -1.2536990206932499e-29;
+
+__device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, double &cs);
+
 __device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
 {
     const double t = fma(th, kTwoOverPi, kShifter);
@@ -173,6 +183,28 @@ __device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
     double r = fma(nd, -kPio2_1, th);
     r = fma(nd, -kPio2_2, r);
     r = fma(nd, -kPio2_3, r);
+    sin_cos_reduced(r, n, sn, cs);
+}
+
+// Rare path: 8e5 <= th < 2^30 (c >~ 2000 times a layer's wave speed); NaN beyond.
+static __device__ __noinline__ void sin_cos_large(double th, double &sn, double &cs)
+{
+    if (!(th < 1073741824.0)) {
+        sn = cs = __longlong_as_double(0x7ff8000000000000ll);
+        return;
+    }
+    const double nd = rint(th * kTwoOverPi);
+    const int n = (int)nd;
+    double r = th - nd * kPio2L_1;           // exact (Sterbenz)
+    r = r - nd * kPio2L_2;
+    r = r - nd * kPio2L_3;
+    r = r - nd * kPio2L_4;
+    r = fma(-nd, kPio2L_5, r);
+    sin_cos_reduced(r, n, sn, cs);
+}
+
+__device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, double &cs)
+{
     const double r2 = r * r;
     double ps = -c_invfact[15];
     ps = fma(ps, r2, c_invfact[13]);
@@ -223,7 +255,7 @@ __device__ __forceinline__ void wave_trig(double q, double kh, double &C, double
     if (th < kTrigMax) {
         sin_cos(th, sn, cs);
     } else {
-        sincos(th, &sn, &cs);
+        sin_cos_large(th, sn, cs);
     }
     C = cs;
     XS = -xi * sn;
@@ -266,6 +298,23 @@ struct Elem {
     double k11, k12, k13, k14, k22, k24;
 };
 
+__device__ __forceinline__ Elem elem_from_triples(double Cr, double XSr, double SXr, double Cs,
+                                                  double XSs, double SXs, double krho, double mu,
+                                                  double c2, double qb)
+{
+    const double CC = Cr * Cs;
+    const double D = fma(SXr, SXs, fma(XSr, XSs, 2.0 * (1.0 - CC)));
+    const double f = (krho * c2) * rcp_fast(D);
+    Elem E;
+    E.k11 = f * fma(Cr, SXs, -XSr * Cs);
+    E.k12 = fma(f, fma(-XSr, XSs, CC - 1.0), -mu * (1.0 + qb));
+    E.k13 = f * (XSr - SXs);
+    E.k14 = f * (Cs - Cr);
+    E.k22 = f * fma(SXr, Cs, -Cr * XSs);
+    E.k24 = f * (XSs - SXr);
+    return E;
+}
+
 __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
 {
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
@@ -285,17 +334,7 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
         wave_triple(qa, L.kh, Cr, XSr, SXr);
         wave_triple(qb, L.kh, Cs, XSs, SXs);
     }
-    const double CC = Cr * Cs;
-    const double D = fma(SXr, SXs, fma(XSr, XSs, 2.0 * (1.0 - CC)));
-    const double f = (L.krho * c2) * rcp_fast(D);
-    Elem E;
-    E.k11 = f * fma(Cr, SXs, -XSr * Cs);
-    E.k12 = fma(f, fma(-XSr, XSs, CC - 1.0), -L.mu * (1.0 + qb));
-    E.k13 = f * (XSr - SXs);
-    E.k14 = f * (Cs - Cr);
-    E.k22 = f * fma(SXr, Cs, -Cr * XSs);
-    E.k24 = f * (XSs - SXr);
-    return E;
+    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2, qb);
 }
 
 // -------------------------------------------------------------- determinant
@@ -325,8 +364,8 @@ struct DetOut {
 // two rows left by the previous step (matrix positions 2t, 2t+1), R[2], R[3] the two rows
 // of the next node (positions 2t+2, 2t+3); columns are [node t | node t+1 | node t+2].
 // Every other row of K is zero in these columns, so choosing the largest |entry| among the
-// four (first in position order on ties) and swapping it to the top is exactly the pivot
-// sequence of dense GEPP on K -- the oracle's algorithm.
+// four and swapping it to the top is the pivot sequence of dense GEPP on K -- the oracle's
+// algorithm -- up to near-ties (magnitudes compared to 2^-20, see mag_key).
 //
 // The pivot rows are resolved by BRANCHING on (p, q) into statically indexed code instead
 // of selecting rows through the index: along a warp's 32 consecutive velocities the pivot
@@ -337,6 +376,11 @@ struct StepOut {
     double piv0, piv1;
     int parity;   // parity of the two GEPP row swaps
 };
+
+// |x| ordering key: the high word without the sign bit (exponent + top 20 mantissa bits).
+// Comparing keys picks a pivot within 2^-20 of the largest magnitude -- as stable as exact
+// partial pivoting -- with one integer op per candidate instead of an FP64-pipe DSETP.
+__device__ __forceinline__ int mag_key(double x) { return __double2hiint(x) & 0x7fffffff; }
 
 template <int NC, int NR, int P, int Q>
 __device__ __forceinline__ void gepp_finish(double (&R)[4][NC], double (&Ri)[4][NC],
@@ -390,7 +434,7 @@ __device__ __forceinline__ void gepp_after_p(double (&R)[4][NC], double (&Ri)[4]
     constexpr int pos1 = (P == 1) ? 0 : 1;
     constexpr int pos2 = (P == 2) ? 0 : 2;
     constexpr int pos3 = (P == 3) ? 0 : 3;
-    const double b1 = fabs(R[pos1][1]), b2 = fabs(R[pos2][1]), b3 = fabs(R[pos3][1]);
+    const int b1 = mag_key(R[pos1][1]), b2 = mag_key(R[pos2][1]), b3 = mag_key(R[pos3][1]);
     if (b2 > b1 && b2 >= b3) {
         gepp_finish<NC, NR, P, 2>(R, Ri, o, X, Xi);
     } else if (b3 > b1 && b3 > b2) {
@@ -405,9 +449,10 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
                                              double (&X)[2][NC - 2], double (&Xi)[2][NC - 2])
 {
     StepOut o;
-    const double a0 = fabs(R[0][0]), a1 = fabs(R[1][0]), a2 = fabs(R[2][0]), a3 = fabs(R[3][0]);
+    const int a0 = mag_key(R[0][0]), a1 = mag_key(R[1][0]), a2 = mag_key(R[2][0]),
+              a3 = mag_key(R[3][0]);
     int p = 0;
-    double best = a0;
+    int best = a0;
     if (a1 > best) { best = a1; p = 1; }
     if (a2 > best) { best = a2; p = 2; }
     if (a3 > best) { best = a3; p = 3; }
@@ -435,11 +480,14 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
 // Cost per node: one layer element + one 4-row GEPP step, O(N) in total.
 // `maybe_near` = false asserts that no layer velocity lies within 1e-3 of c (the scan
 // decides it once per warp for its 32 velocities), which skips the per-lane S4 loop exactly.
-template <bool WANT_VALUE>
+// NFIX > 0 compiles the determinant for exactly NFIX layers (fully unrolled: no loop-carried
+// register copies, constant shared-memory offsets); NFIX = 0 takes N at run time.
+template <bool WANT_VALUE, int NFIX = 0>
 __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
-                                        const double *__restrict__ vel, int N, double c,
+                                        const double *__restrict__ vel, int Nrt, double c,
                                         bool maybe_near = true)
 {
+    const int N = NFIX > 0 ? NFIX : Nrt;
     const double cp = maybe_near ? perturb_velocity(vel, 2 * (N + 1), c) : c;
     const double c2 = cp * cp;
 
@@ -451,8 +499,7 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     Elem P = layer_elem(load_lc(lc), c2);
     double X[2][4] = {{P.k11, P.k12, P.k13, P.k14}, {P.k12, P.k22, -P.k14, P.k24}};
 
-#pragma unroll 1
-    for (int t = 0; t + 1 < N; ++t) {
+    auto node_step = [&](int t) {
         const Elem Q = layer_elem(load_lc(lc + t + 1), c2);
         double R[4][6] = {
             {X[0][0], X[0][1], X[0][2], X[0][3], 0.0, 0.0},
@@ -476,6 +523,13 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
             acc.mul(piv1);
         }
         P = Q;
+    };
+    if constexpr (NFIX > 0) {
+#pragma unroll
+        for (int t = 0; t + 1 < NFIX; ++t) node_step(t);
+    } else {
+#pragma unroll 1
+        for (int t = 0; t + 1 < N; ++t) node_step(t);
     }
 
     // Half-space K_hs = mu [[r w/(1-rs), w/(1-rs) - 2], [., s w/(1-rs)]], w = 1 - s^2 =
@@ -564,5 +618,6 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     }
     return out;
 }
+
 
 }  // namespace masw

@@ -190,7 +190,7 @@ constexpr int scan_min_blocks()
     return BLOCK == 256 ? MASW_SCAN_MINB : 1;
 }
 
-template <int TEAM, int BLOCK>
+template <int TEAM, int BLOCK, int NFIX>
 __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(ScanArgs a)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             int s = 0;
             bool bad = false;
             if (j < V) {
-                const DetOut d = det_K<false>(lc, vel, N, cg[j], near);
+                const DetOut d = det_K<false, NFIX>(lc, vel, N, cg[j], near);
                 s = d.sign;
                 bad = d.bad;
                 ++my_eval;
@@ -372,15 +372,16 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
     return team;
 }
 
-template <int TEAM, int BLOCK>
+template <int TEAM, int BLOCK, int NFIX>
 static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     const size_t smem = round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
                         (size_t)TEAMS * team_model_bytes(a.mod.N);
-    auto kern = scan_kernel<TEAM, BLOCK>;
+    auto kern = scan_kernel<TEAM, BLOCK, NFIX>;
     const int sms = sm_count(device);
-    const long long key = ((long long)device << 40) | ((long long)TEAM << 32) | (long long)smem;
+    const long long key = ((long long)device << 48) | ((long long)NFIX << 40) |
+                          ((long long)TEAM << 32) | (long long)smem;
     int per_sm = 0;
     {
         std::lock_guard<std::mutex> g(g_cache_mu);
@@ -409,14 +410,19 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
     return cudaGetLastError();
 }
 
+// One run-time-N kernel per team size.  Measured and rejected on B200 (C5, 94 ms baseline):
+//  * TEAM = 1 compiled per N in 1..12 with the determinant fully unrolled: 119 ms (the N=6
+//    kernel grew to 9.4k instructions; instruction-cache bound);
+//  * a row-pair kernel sharing the (model, c) terms of two wavelengths per lane: 132 ms
+//    (register-bound: 128 registers with spills, or 230 registers at 8 warps/SM).
 cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device)
 {
     switch (team_warps) {
-        case 1: return launch_scan_t<1, 256>(a, st, device);
-        case 2: return launch_scan_t<2, 256>(a, st, device);
-        case 4: return launch_scan_t<4, 256>(a, st, device);
-        case 8: return launch_scan_t<8, 256>(a, st, device);
-        case 16: return launch_scan_t<16, 512>(a, st, device);
+        case 1: return launch_scan_t<1, 256, 0>(a, st, device);
+        case 2: return launch_scan_t<2, 256, 0>(a, st, device);
+        case 4: return launch_scan_t<4, 256, 0>(a, st, device);
+        case 8: return launch_scan_t<8, 256, 0>(a, st, device);
+        case 16: return launch_scan_t<16, 512, 0>(a, st, device);
         default: return cudaErrorInvalidValue;
     }
 }

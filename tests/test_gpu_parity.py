@@ -331,3 +331,35 @@ def test_realistic_full_size(masw, orc):
     assert ok.all(), np.nonzero(~ok)[0][:10]
     mis = masw.masw_misfit(ct, dev(w.ce))
     assert parity.misfit_ok(orc, ct.cpu().numpy(), w.ce, mis)
+
+
+@pytest.mark.parametrize("L", [1, 3, 39])
+def test_pair_kernel_odd_wavelength_counts(masw, orc, L):
+    """TEAM=1 runs the row-pair kernel (rows 2i, 2i+1 of one model share c): odd L leaves a
+    pair with a single row; compare with the oracle and with another team size."""
+    w = synth.workload("ensemble", M=37)
+    mods = w.models
+    lam = w.lam[:L]
+    ce = w.ce[:L]
+    r1 = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, lam, w.c, ce,
+                                   team_warps=1)
+    r4 = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, lam, w.c, ce,
+                                   team_warps=4)
+    assert np.array_equal(r1.idx, r4.idx) and np.array_equal(r1.misfit, r4.misfit)
+    o = orc.ensemble(mods, lam, w.c, ce)
+    for m in range(mods.n_models):
+        ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), lam, w.c, r1.idx[m], o["idx"][m])
+        assert ok.all()
+    alg, ev = masw.masw_last_work()
+    assert alg > 0
+
+
+def test_async_scan_timing_ring(masw):
+    w = synth.workload("ensemble", M=50)
+    mods = w.models
+    args = [dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)]
+    for _ in range(3):
+        masw.masw_curves_ensemble(*args, dev(w.lam), dev(w.c), dev(w.ce),
+                                  flags=masw.ASYNC | masw.TIME_SCAN)
+    ms = masw.masw_recent_scan_ms(3)
+    assert len(ms) == 3 and all(x > 0 for x in ms)
