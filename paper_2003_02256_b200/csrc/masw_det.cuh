@@ -126,11 +126,12 @@ __device__ __forceinline__ double scale2(double x, int k)
 }
 
 // cosh and sinh of th in [0, 700] without branches (the caller guarantees th <= 350, range
-// guard S9).  th = n ln2 + r, |r| <= ln2/2, em1 = e^r - 1 by its Taylor series to r^14
-// (no constant term, so it is accurate for tiny r), p = 1 + em1, q = 1/p, and with
-// a = 2^(n-1), b = 2^(-n-1):
-//   cosh = a p + b q
-//   sinh = (a - b) + a em1 + b em1 q        (e^r - e^-r = em1 + em1/p: no cancellation at n=0)
+// guard S9).  th = n ln2 + r, |r| <= ln2/2; the Taylor series of e^r - 1 to r^14 is split
+// into its even part E = r^2/2! + r^4/4! + ... and odd part O = r + r^3/3! + ... (two
+// independent Horner chains in r^2), so e^r - 1 = E + O and e^-r - 1 = E - O need no
+// reciprocal.  With a = 2^(n-1), b = 2^(-n-1):
+//   cosh = (a + b) + a (E + O) + b (E - O)
+//   sinh = (a - b) + a (E + O) - b (E - O)   (= O exactly structured at n = 0: no cancellation)
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
 {
     const double t = fma(th, kLog2e, kShifter);
@@ -138,27 +139,27 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
     const int n = __double2loint(t);
     double r = fma(nd, -kLn2Hi, th);
     r = fma(nd, -kLn2Lo, r);
-    double e = c_invfact[14];
-    e = fma(e, r, c_invfact[13]);
-    e = fma(e, r, c_invfact[12]);
-    e = fma(e, r, c_invfact[11]);
-    e = fma(e, r, c_invfact[10]);
-    e = fma(e, r, c_invfact[9]);
-    e = fma(e, r, c_invfact[8]);
-    e = fma(e, r, c_invfact[7]);
-    e = fma(e, r, c_invfact[6]);
-    e = fma(e, r, c_invfact[5]);
-    e = fma(e, r, c_invfact[4]);
-    e = fma(e, r, c_invfact[3]);
-    e = fma(e, r, 0.5);
-    e = fma(e, r, 1.0);
-    const double em1 = e * r;
-    const double p = 1.0 + em1;
-    const double q = rcp_fast(p);
+    const double r2 = r * r;
+    double pe = c_invfact[14];                 // E / r^2 = 1/2! + r^2/4! + ... + r^12/14!
+    pe = fma(pe, r2, c_invfact[12]);
+    pe = fma(pe, r2, c_invfact[10]);
+    pe = fma(pe, r2, c_invfact[8]);
+    pe = fma(pe, r2, c_invfact[6]);
+    pe = fma(pe, r2, c_invfact[4]);
+    pe = fma(pe, r2, 0.5);
+    double po = c_invfact[13];                 // O / r = 1 + r^2/3! + ... + r^12/13!
+    po = fma(po, r2, c_invfact[11]);
+    po = fma(po, r2, c_invfact[9]);
+    po = fma(po, r2, c_invfact[7]);
+    po = fma(po, r2, c_invfact[5]);
+    po = fma(po, r2, c_invfact[3]);
+    po = fma(po, r2, 1.0);
+    const double E = pe * r2, O = po * r;
     const double a = __hiloint2double((n + 1022) << 20, 0);    // 2^(n-1)
     const double b = __hiloint2double((1022 - n) << 20, 0);    // 2^(-n-1)
-    ch = fma(a, p, b * q);
-    sh = fma(a, em1, fma(b * em1, q, a - b));
+    const double ep = E + O, em = E - O;                       // e^r - 1, e^-r - 1
+    ch = fma(a, ep, fma(b, em, a + b));
+    sh = fma(a, ep, fma(-b, em, a - b));
 }
 
 // sin and cos of th in [0, 8e5] (< 2^19 pi/2: Cody-Waite reduction exact; Taylor on
