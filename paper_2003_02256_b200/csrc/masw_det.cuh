@@ -68,13 +68,22 @@ __device__ __forceinline__ LayerConst load_lc(const LayerConst *p)
 // with polynomial coefficients in the constant bank (DFMA takes them as c[][] operands; the
 // libm versions spend two UMOV issue slots per coefficient).  Each is within ~1-2 ulp.
 //
-// Taylor coefficients 1/k!, k = 0..20, correctly rounded.
-static __constant__ double c_invfact[21] = {
-    1.0, 1.0, 1.0 / 2.0, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0,
-    1.0 / 40320.0, 1.0 / 362880.0, 1.0 / 3628800.0, 1.0 / 39916800.0, 1.0 / 479001600.0,
-    1.0 / 6227020800.0, 1.0 / 87178291200.0, 1.0 / 1307674368000.0, 1.0 / 20922789888000.0,
-    1.0 / 355687428096000.0, 1.0 / 6402373705728000.0, 1.0 / 121645100408832000.0,
-    1.0 / 2432902008176640000.0};
+// Near-minimax (Chebyshev-fitted, coefficients rounded to fp64; scripts/minimax_coeffs.py)
+// polynomials in u = r^2, highest degree first.  Max relative error with these fp64
+// coefficients (50-digit check): e^r even part E/u 4e-19 and odd part O/r 1.4e-18 on
+// |r| <= ln2/2; sin(r)/r 1.3e-17 and cos(r) 7.2e-18 on |r| <= pi/4.
+static __constant__ double c_expE[6] = {2.0918129454967065e-09, 2.755726330147475e-07,
+                                        2.480158733642132e-05, 0.0013888888888879082,
+                                        0.04166666666666668, 0.5};
+static __constant__ double c_expO[6] = {2.5110037605963777e-08, 2.755724091857897e-06,
+                                        0.00019841269890047113, 0.008333333333319601,
+                                        0.1666666666666668, 1.0};
+static __constant__ double c_sin[6] = {1.5894736651849094e-10, -2.5050716974102745e-08,
+                                       2.755731337640013e-06, -0.000198412698286503,
+                                       0.008333333333320363, -0.16666666666666616};
+static __constant__ double c_cos[7] = {-1.1353379638297575e-11, 2.0875582380663952e-09,
+                                       -2.7557313097790086e-07, 2.4801587283881152e-05,
+                                       -0.0013888888888861095, 0.04166666666666645, -0.5};
 
 constexpr double kShifter = 6755399441055744.0;         // 1.5 * 2^52: round-to-integer trick
 constexpr double kLog2e = 1.4426950408889634;
@@ -126,9 +135,9 @@ __device__ __forceinline__ double scale2(double x, int k)
 }
 
 // cosh and sinh of th in [0, 700] without branches (the caller guarantees th <= 350, range
-// guard S9).  th = n ln2 + r, |r| <= ln2/2; the Taylor series of e^r - 1 to r^14 is split
-// into its even part E = r^2/2! + r^4/4! + ... and odd part O = r + r^3/3! + ... (two
-// independent Horner chains in r^2), so e^r - 1 = E + O and e^-r - 1 = E - O need no
+// guard S9).  th = n ln2 + r, |r| <= ln2/2; e^r - 1 is split into its even part
+// E = r^2/2! + r^4/4! + ... and odd part O = r + r^3/3! + ... (two independent Horner
+// chains in r^2, near-minimax degree 5), so e^r - 1 = E + O and e^-r - 1 = E - O need no
 // reciprocal.  With a = 2^(n-1), b = 2^(-n-1):
 //   cosh = (a + b) + a (E + O) + b (E - O)
 //   sinh = (a - b) + a (E + O) - b (E - O)   (= O exactly structured at n = 0: no cancellation)
@@ -140,20 +149,13 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
     double r = fma(nd, -kLn2Hi, th);
     r = fma(nd, -kLn2Lo, r);
     const double r2 = r * r;
-    double pe = c_invfact[14];                 // E / r^2 = 1/2! + r^2/4! + ... + r^12/14!
-    pe = fma(pe, r2, c_invfact[12]);
-    pe = fma(pe, r2, c_invfact[10]);
-    pe = fma(pe, r2, c_invfact[8]);
-    pe = fma(pe, r2, c_invfact[6]);
-    pe = fma(pe, r2, c_invfact[4]);
-    pe = fma(pe, r2, 0.5);
-    double po = c_invfact[13];                 // O / r = 1 + r^2/3! + ... + r^12/13!
-    po = fma(po, r2, c_invfact[11]);
-    po = fma(po, r2, c_invfact[9]);
-    po = fma(po, r2, c_invfact[7]);
-    po = fma(po, r2, c_invfact[5]);
-    po = fma(po, r2, c_invfact[3]);
-    po = fma(po, r2, 1.0);
+    double pe = c_expE[0];                     // E / r^2  (~ 1/2! + r^2/4! + ...)
+    double po = c_expO[0];                     // O / r    (~ 1 + r^2/3! + ...)
+#pragma unroll
+    for (int i = 1; i < 6; ++i) {
+        pe = fma(pe, r2, c_expE[i]);
+        po = fma(po, r2, c_expO[i]);
+    }
     const double E = pe * r2, O = po * r;
     const double a = __hiloint2double((n + 1022) << 20, 0);    // 2^(n-1)
     const double b = __hiloint2double((1022 - n) << 20, 0);    // 2^(-n-1)
@@ -162,8 +164,8 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
     sh = fma(a, ep, fma(-b, em, a - b));
 }
 
-// sin and cos of th in [0, 8e5] (< 2^19 pi/2: Cody-Waite reduction exact; Taylor on
-// |r| <= pi/4: sin to r^15, cos to r^16, truncation < 1e-16).  No branches; the caller
+// sin and cos of th in [0, 8e5] (< 2^19 pi/2: Cody-Waite reduction exact; near-minimax
+// polynomials on |r| <= pi/4: sin to r^13, cos to r^14).  No branches; the caller
 // routes larger arguments to sin_cos_large.
 constexpr double kTrigMax = 8.0e5;
 // pi/2 in five parts, the first four of <= 23 significant bits: n * part is exact for
@@ -207,22 +209,15 @@ static __device__ __noinline__ void sin_cos_large(double th, double &sn, double 
 __device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, double &cs)
 {
     const double r2 = r * r;
-    double ps = -c_invfact[15];
-    ps = fma(ps, r2, c_invfact[13]);
-    ps = fma(ps, r2, -c_invfact[11]);
-    ps = fma(ps, r2, c_invfact[9]);
-    ps = fma(ps, r2, -c_invfact[7]);
-    ps = fma(ps, r2, c_invfact[5]);
-    ps = fma(ps, r2, -c_invfact[3]);
+    double ps = c_sin[0];
+    double pc = c_cos[0];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) {
+        ps = fma(ps, r2, c_sin[i]);
+        pc = fma(pc, r2, c_cos[i]);
+    }
+    pc = fma(pc, r2, c_cos[6]);
     const double s = fma(r * r2, ps, r);
-    double pc = c_invfact[16];
-    pc = fma(pc, r2, -c_invfact[14]);
-    pc = fma(pc, r2, c_invfact[12]);
-    pc = fma(pc, r2, -c_invfact[10]);
-    pc = fma(pc, r2, c_invfact[8]);
-    pc = fma(pc, r2, -c_invfact[6]);
-    pc = fma(pc, r2, c_invfact[4]);
-    pc = fma(pc, r2, -0.5);
     const double c = fma(r2, pc, 1.0);
     // quadrant n mod 4: (sin, cos) = (s, c), (c, -s), (-s, -c), (-c, s)
     const bool swap = n & 1;
