@@ -108,21 +108,22 @@ def uniform_model() -> Models:
 
 
 def ensemble_models(M: int = 100_000, seed: int = ENSEMBLE_SEED) -> Models:
-    """C5: M random 6-layer models, PCG64(seed); draw order β, h, ρ (each [M][·]).
+    """C5: M random 6-layer models, PCG64(seed).
 
-    β_e = β_ref,e·U(0.6,1.4), h_e = h_ref,e·U(0.5,1.5), α = 1440, ρ_e = U(1700,2000).
-    Velocity reversals are allowed.  Any prefix of a larger ensemble is bit-identical.
+    Each model draws 20 uniforms u in [0, 1) in order (row-major over models, so any prefix
+    of a larger ensemble is bit-identical): β_e = β_ref,e·(0.6 + 0.8 u_e) (e < 7),
+    h_e = h_ref,e·(0.5 + u_{7+e}) (e < 6), ρ_e = 1700 + 300 u_{13+e} (e < 7); α = 1440.
+    Velocity reversals are allowed.
     """
     beta_ref = np.array([75.0, 90.0, 150.0, 180.0, 240.0, 290.0, 290.0])
     h_ref = np.array([1.0, 1.0, 2.0, 2.0, 4.0, 5.0])
     rng = np.random.Generator(np.random.PCG64(seed))
-    ub = rng.uniform(0.6, 1.4, size=(M, 7))
-    uh = rng.uniform(0.5, 1.5, size=(M, 6))
-    rho = rng.uniform(1700.0, 2000.0, size=(M, 7))
-    beta = np.ascontiguousarray(beta_ref[None, :] * ub)
-    h = np.ascontiguousarray(h_ref[None, :] * uh)
+    u = rng.random((M, 20))
+    beta = np.ascontiguousarray(beta_ref[None, :] * (0.6 + 0.8 * u[:, 0:7]))
+    h = np.ascontiguousarray(h_ref[None, :] * (0.5 + u[:, 7:13]))
+    rho = np.ascontiguousarray(1700.0 + 300.0 * u[:, 13:20])
     alpha = np.full((M, 7), 1440.0)
-    return Models(h, alpha, beta, np.ascontiguousarray(rho))
+    return Models(h, alpha, beta, rho)
 
 
 def tiny_lambdas() -> np.ndarray:
