@@ -68,6 +68,11 @@ def lib():
             L.oracle_det_grid_ld.argtypes = [ctypes.c_int32, _D, _D, _D, _D, _D, ctypes.c_int64,
                                              _D, ctypes.c_int64, _D, _D, _I32, _I32,
                                              ctypes.c_int32]
+            L.oracle_det_kappa.argtypes = [ctypes.c_int32, _D, _D, _D, _D, ctypes.c_double,
+                                           ctypes.c_double, _D]
+            L.oracle_det_grid_kappa.argtypes = [ctypes.c_int32, _D, _D, _D, _D, _D,
+                                                ctypes.c_int64, _D, ctypes.c_int64, _D, _I32,
+                                                ctypes.c_int32]
             L.oracle_curve.argtypes = [ctypes.c_int32, _D, _D, _D, _D, _D, ctypes.c_int64, _D,
                                        ctypes.c_int64, _D, _I32, _I64, ctypes.c_int32]
             L.oracle_misfit.argtypes = [_D, _D, ctypes.c_int64, _D]
@@ -163,6 +168,30 @@ def det(h, alpha, beta, rho, lam, c, extended: bool = False):
     fn = lib().oracle_det_ld if extended else lib().oracle_det
     st = fn(N, *[p for _, p in args], float(lam), float(c), m.ctypes.data_as(_D), ctypes.byref(e))
     return complex(m[0], m[1]), int(e.value), st
+
+
+def det_kappa(h, alpha, beta, rho, lam, c):
+    """Conditioning of det K w.r.t. 1-ulp errors in the per-layer cosh/sinh/sqrt values
+    (reading S15'): relative det change bound, from long-double finite differences."""
+    N = len(h)
+    args = [_d(x) for x in (h, alpha, beta, rho)]
+    out = ctypes.c_double(0.0)
+    lib().oracle_det_kappa(N, *[p for _, p in args], float(lam), float(c), ctypes.byref(out))
+    return out.value
+
+
+def det_grid_kappa(h, alpha, beta, rho, lam, c, nthreads: int | None = None):
+    """det_kappa on the full (λ, c) grid → kappa[L][V]."""
+    N = len(h)
+    args = [_d(x) for x in (h, alpha, beta, rho)]
+    lam, plam = _d(lam)
+    c, pc = _d(c)
+    L, V = len(lam), len(c)
+    kap = np.zeros((L, V))
+    sts = np.zeros((L, V), dtype=np.int32)
+    lib().oracle_det_grid_kappa(N, *[p for _, p in args], plam, L, pc, V, kap.ctypes.data_as(_D),
+                                sts.ctypes.data_as(_I32), nthreads or default_threads())
+    return kap
 
 
 # ---------------------------------------------------------------- O7..O10

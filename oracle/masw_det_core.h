@@ -31,13 +31,22 @@
  *   Ke = [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12], [k14, k24, -k12, k22]]
  * Local DOFs (u_top, w_top, u_bot, w_bot).
  */
+/* pw >= 0 multiplies one intermediate value by pf (0: Cr, 1: Sr, 2: Cs, 3: Ss, 4: r, 5: s)
+ * -- used only by the conditioning measure (reading S15'); pw < 0 leaves the arithmetic
+ * untouched. */
 static void OR_NAME(layer_element)(REAL h, REAL alpha, REAL beta, REAL rho, REAL k, REAL c,
-                                   CREAL_T Ke[4][4])
+                                   CREAL_T Ke[4][4], int pw, REAL pf)
 {
     CREAL_T r = sqrt((CREAL_T)(1.0 - (c * c) / (alpha * alpha)));
     CREAL_T s = sqrt((CREAL_T)(1.0 - (c * c) / (beta * beta)));
+    if (pw == 4) r = r * pf;
+    if (pw == 5) s = s * pf;
     CREAL_T Cr = cosh(k * r * h), Sr = sinh(k * r * h);
     CREAL_T Cs = cosh(k * s * h), Ss = sinh(k * s * h);
+    if (pw == 0) Cr = Cr * pf;
+    if (pw == 1) Sr = Sr * pf;
+    if (pw == 2) Cs = Cs * pf;
+    if (pw == 3) Ss = Ss * pf;
     CREAL_T D = 2.0 * (1.0 - Cr * Cs) + (1.0 / (r * s) + r * s) * Sr * Ss;
     CREAL_T f = k * rho * c * c / D;
     CREAL_T k11 = f * (Cr * Ss / s - r * Sr * Cs);
@@ -59,10 +68,12 @@ static void OR_NAME(layer_element)(REAL h, REAL alpha, REAL beta, REAL rho, REAL
  * (reading S1, S22.)
  */
 static void OR_NAME(halfspace_element)(REAL alpha, REAL beta, REAL rho, REAL k, REAL c,
-                                       CREAL_T Kh[2][2])
+                                       CREAL_T Kh[2][2], int pw, REAL pf)
 {
     CREAL_T r = sqrt((CREAL_T)(1.0 - (c * c) / (alpha * alpha)));
     CREAL_T s = sqrt((CREAL_T)(1.0 - (c * c) / (beta * beta)));
+    if (pw == 4) r = r * pf;
+    if (pw == 5) s = s * pf;
     REAL mu = k * rho * beta * beta;
     CREAL_T q = (1.0 - s * s) / (1.0 - r * s);
     Kh[0][0] = mu * r * q;
@@ -74,20 +85,22 @@ static void OR_NAME(halfspace_element)(REAL alpha, REAL beta, REAL rho, REAL k, 
 /* Dense global assembly: layer e adds Ke into rows/cols 2e..2e+3, the half-space adds
  * K_hs into rows/cols 2N, 2N+1 (PAPER.md:78 order 2(N+1)).  c is used as
  * given (callers pass the perturbed c'). */
+/* pe: element whose intermediate value pw is scaled by pf (pe == N: the half-space, pw 4/5);
+ * pe < 0: no perturbation (the oracle proper). */
 static void OR_NAME(assemble)(int32_t N, const double *h, const double *alpha,
                               const double *beta, const double *rho, double k, double c,
-                              CREAL_T *K /* [n*n] */)
+                              CREAL_T *K /* [n*n] */, int pe, int pw, REAL pf)
 {
     int n = 2 * (N + 1);
     for (int i = 0; i < n * n; ++i) K[i] = 0.0;
     for (int e = 0; e < N; ++e) {
         CREAL_T Ke[4][4];
-        OR_NAME(layer_element)(h[e], alpha[e], beta[e], rho[e], k, c, Ke);
+        OR_NAME(layer_element)(h[e], alpha[e], beta[e], rho[e], k, c, Ke, e == pe ? pw : -1, pf);
         for (int a = 0; a < 4; ++a)
             for (int b = 0; b < 4; ++b) K[(2 * e + a) * n + (2 * e + b)] += Ke[a][b];
     }
     CREAL_T Kh[2][2];
-    OR_NAME(halfspace_element)(alpha[N], beta[N], rho[N], k, c, Kh);
+    OR_NAME(halfspace_element)(alpha[N], beta[N], rho[N], k, c, Kh, pe == N ? pw : -1, pf);
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) K[(2 * N + a) * n + (2 * N + b)] += Kh[a][b];
 }
@@ -151,14 +164,21 @@ static int OR_NAME(det_lu)(int n, CREAL_T *A, CREAL_T *mant, int *exp2)
 }
 
 /* O1-O5 for one (model, lambda, c): k, perturb, assemble, dense det. */
+static int OR_NAME(det_at_p)(int32_t N, const double *h, const double *alpha,
+                             const double *beta, const double *rho, double lambda, double c,
+                             CREAL_T *K, CREAL_T *mant, int *exp2, int pe, int pw, REAL pf)
+{
+    double k = OR_TWO_PI / lambda;
+    double cp = oracle_perturb_velocity(N, alpha, beta, c);
+    OR_NAME(assemble)(N, h, alpha, beta, rho, k, cp, K, pe, pw, pf);
+    return OR_NAME(det_lu)(2 * (N + 1), K, mant, exp2);
+}
+
 static int OR_NAME(det_at)(int32_t N, const double *h, const double *alpha, const double *beta,
                            const double *rho, double lambda, double c, CREAL_T *K,
                            CREAL_T *mant, int *exp2)
 {
-    double k = OR_TWO_PI / lambda;
-    double cp = oracle_perturb_velocity(N, alpha, beta, c);
-    OR_NAME(assemble)(N, h, alpha, beta, rho, k, cp, K);
-    return OR_NAME(det_lu)(2 * (N + 1), K, mant, exp2);
+    return OR_NAME(det_at_p)(N, h, alpha, beta, rho, lambda, c, K, mant, exp2, -1, -1, 1.0);
 }
 
 #undef OR_CAT2

@@ -158,7 +158,7 @@ void oracle_layer_element(double h, double alpha, double beta, double rho, doubl
                           double *out32)
 {
     cplx Ke[4][4];
-    layer_element_d(h, alpha, beta, rho, k, c, Ke);
+    layer_element_d(h, alpha, beta, rho, k, c, Ke, -1, 1.0);
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
             out32[2 * (4 * a + b)] = creal(Ke[a][b]);
@@ -170,7 +170,7 @@ void oracle_halfspace_element(double alpha, double beta, double rho, double k, d
                               double *out8)
 {
     cplx Kh[2][2];
-    halfspace_element_d(alpha, beta, rho, k, c, Kh);
+    halfspace_element_d(alpha, beta, rho, k, c, Kh, -1, 1.0);
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {
             out8[2 * (2 * a + b)] = creal(Kh[a][b]);
@@ -183,7 +183,7 @@ void oracle_assemble(int32_t N, const double *h, const double *alpha, const doub
 {
     int n = 2 * (N + 1);
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
-    assemble_d(N, h, alpha, beta, rho, k, c, K);
+    assemble_d(N, h, alpha, beta, rho, k, c, K, -1, -1, 1.0);
     for (int i = 0; i < n * n; ++i) {
         out[2 * i] = creal(K[i]);
         out[2 * i + 1] = cimag(K[i]);
@@ -219,6 +219,58 @@ int oracle_det(int32_t N, const double *h, const double *alpha, const double *be
     mant2[1] = cimag(m);
     *exp2 = e;
     return st;
+}
+
+/* Conditioning of det K with respect to the rounding of the elementary-function values that
+ * every fp64 evaluation of the Kausel-Roesset formulas must compute (reading S15'):
+ *   kappa = 2^-53 * sum over layers e, values v in {cosh, sinh of both waves, r, s} (and r, s
+ *           of the half-space) of |d ln det / d ln v|,
+ * i.e. the first-order relative change of det K when each such value is off by one unit
+ * roundoff.  Derivatives by finite differences (relative step 2^-30) in long double. */
+static long double det_ld_value(int32_t N, const double *h, const double *alpha,
+                                const double *beta, const double *rho, double lambda,
+                                double c, cplx_ld *K, int pe, int pw, long double pf, int *st,
+                                cplx_ld *m_out, int *e_out)
+{
+    cplx_ld m = 0.0;
+    int e = 0;
+    *st = det_at_p_ld(N, h, alpha, beta, rho, lambda, c, K, &m, &e, pe, pw, pf);
+    *m_out = m;
+    *e_out = e;
+    return 0.0L;
+}
+
+int oracle_det_kappa(int32_t N, const double *h, const double *alpha, const double *beta,
+                     const double *rho, double lambda, double c, double *kappa)
+{
+    int n = 2 * (N + 1);
+    cplx_ld *K = (cplx_ld *)malloc(sizeof(cplx_ld) * n * n);
+    cplx_ld m0, m1;
+    int e0, e1, st;
+    det_ld_value(N, h, alpha, beta, rho, lambda, c, K, -1, -1, 1.0L, &st, &m0, &e0);
+    if (st != OR_OK || creall(m0) == 0.0L) {
+        free(K);
+        *kappa = INFINITY;
+        return st;
+    }
+    const long double step = ldexpl(1.0L, -30), unit = ldexpl(1.0L, -53);
+    long double sum = 0.0L;
+    for (int pe = 0; pe <= N; ++pe) {
+        for (int pw = (pe == N ? 4 : 0); pw < 6; ++pw) {
+            det_ld_value(N, h, alpha, beta, rho, lambda, c, K, pe, pw, 1.0L + step, &st, &m1, &e1);
+            if (st != OR_OK) {
+                free(K);
+                *kappa = INFINITY;
+                return st;
+            }
+            /* d = (m1 2^e1 - m0 2^e0) / (m0 2^e0) */
+            cplx_ld ratio = (m1 / m0) * ldexpl(1.0L, e1 - e0);
+            sum += cabsl(ratio - 1.0L) / step;
+        }
+    }
+    free(K);
+    *kappa = (double)(sum * unit);
+    return OR_OK;
 }
 
 /* The same determinant carried in long double (reading S15'): mantissa rounded to double. */
@@ -455,7 +507,7 @@ typedef struct {
     int64_t L, V;
     double *mre, *mim;
     int32_t *ex, *status;
-    int extended; /* 1: long double audit instance (reading S15') */
+    int extended; /* 1: long double audit instance, 2: conditioning kappa (reading S15') */
     atomic_llong next;
 } grid_job;
 
@@ -471,7 +523,12 @@ static void *grid_worker(void *arg)
         for (int64_t j = 0; j < G->V; ++j) {
             double re, im;
             int e = 0, st;
-            if (G->extended) {
+            if (G->extended == 2) {
+                double kap = 0.0;
+                st = oracle_det_kappa(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], &kap);
+                re = kap;
+                im = 0.0;
+            } else if (G->extended) {
                 cplx_ld m = 0.0;
                 st = det_at_ld(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], Kl, &m, &e);
                 re = (double)creall(m);
@@ -506,6 +563,20 @@ int oracle_det_grid(int32_t N, const double *h, const double *alpha, const doubl
 {
     return det_grid_impl(0, N, h, alpha, beta, rho, lam, L, c, V, mant_re, mant_im, exp2,
                          status, nthreads);
+}
+
+/* kappa (oracle_det_kappa) on the grid, written to mant_re (reading S15'). */
+int oracle_det_grid_kappa(int32_t N, const double *h, const double *alpha, const double *beta,
+                          const double *rho, const double *lam, int64_t L, const double *c,
+                          int64_t V, double *kappa, int32_t *status, int32_t nthreads)
+{
+    double *im = (double *)malloc(sizeof(double) * L * V);
+    int32_t *ex = (int32_t *)malloc(sizeof(int32_t) * L * V);
+    int st = det_grid_impl(2, N, h, alpha, beta, rho, lam, L, c, V, kappa, im, ex, status,
+                           nthreads);
+    free(im);
+    free(ex);
+    return st;
 }
 
 /* The grid in long double (reading S15': measures the fp64 oracle's rounding error). */

@@ -311,6 +311,14 @@ __device__ __forceinline__ Elem elem_from_triples(double Cr, double XSr, double 
     return E;
 }
 
+// Rare case c > alpha_e (both waves possibly trigonometric): kept out of line so the hot
+// loop's code stays small (instruction-cache pressure was measured: no_instruction stalls).
+static __device__ __noinline__ void waves_general(double qa, double qb, double kh, double *t)
+{
+    wave_triple(qa, kh, t[0], t[1], t[2]);
+    wave_triple(qb, kh, t[3], t[4], t[5]);
+}
+
 __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
 {
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
@@ -327,8 +335,10 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
             wave_trig(qb, L.kh, Cs, XSs, SXs);
         }
     } else {
-        wave_triple(qa, L.kh, Cr, XSr, SXr);
-        wave_triple(qb, L.kh, Cs, XSs, SXs);
+        double t[6];
+        waves_general(qa, qb, L.kh, t);
+        Cr = t[0]; XSr = t[1]; SXr = t[2];
+        Cs = t[3]; XSs = t[4]; SXs = t[5];
     }
     return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2, qb);
 }

@@ -356,6 +356,79 @@ def test_P9_extended_audit_is_accurate(orc):
     assert worst_fp64 > 1e-10      # the audit matters: fp64 alone is not 1e-10-accurate here
 
 
+def _mp_det_pert(h, alpha, beta, rho, lam, c, pe, pw, eps, dps=40):
+    """50-digit det K with one intermediate value of element pe scaled by (1 + eps):
+    pw 0..3 = cosh/sinh of the P and S waves (Cr, Sr, Cs, Ss), 4/5 = r/s (pe == N: half-space)."""
+    import mpmath as mp
+
+    mp.mp.dps = dps
+    N = len(h)
+    n = 2 * (N + 1)
+    k = mp.mpf(6.283185307179586 / lam)
+    c = mp.mpf(c)
+    K = mp.matrix(n, n)
+    for e in range(N + 1):
+        al, be, rh = mp.mpf(alpha[e]), mp.mpf(beta[e]), mp.mpf(rho[e])
+        r = mp.sqrt(mp.mpc(1 - c * c / al ** 2))
+        s = mp.sqrt(mp.mpc(1 - c * c / be ** 2))
+        if e == pe and pw == 4:
+            r *= 1 + eps
+        if e == pe and pw == 5:
+            s *= 1 + eps
+        if e == N:
+            mu = k * rh * be * be
+            q = (1 - s * s) / (1 - r * s)
+            K[2 * N, 2 * N] += mu * r * q
+            K[2 * N, 2 * N + 1] += mu * q - 2 * mu
+            K[2 * N + 1, 2 * N] += mu * q - 2 * mu
+            K[2 * N + 1, 2 * N + 1] += mu * s * q
+            continue
+        he = mp.mpf(h[e])
+        v = [mp.cosh(k * r * he), mp.sinh(k * r * he), mp.cosh(k * s * he), mp.sinh(k * s * he)]
+        if e == pe and pw < 4:
+            v[pw] *= 1 + eps
+        Cr, Sr, Cs, Ss = v
+        D = 2 * (1 - Cr * Cs) + (1 / (r * s) + r * s) * Sr * Ss
+        f = k * rh * c * c / D
+        k11 = f * (Cr * Ss / s - r * Sr * Cs)
+        k12 = f * (Cr * Cs - r * s * Sr * Ss - 1) - k * rh * be * be * (1 + s * s)
+        k13 = f * (r * Sr - Ss / s)
+        k14 = f * (Cs - Cr)
+        k22 = f * (Sr * Cs / r - s * Cr * Ss)
+        k24 = f * (s * Ss - Sr / r)
+        Ke = [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12], [k14, k24, -k12, k22]]
+        for a_ in range(4):
+            for b_ in range(4):
+                K[2 * e + a_, 2 * e + b_] += Ke[a_][b_]
+    return mp.det(K)
+
+
+def test_P9_kappa_matches_mpmath_sensitivity(orc):
+    """kappa (reading S15') = 2^-53 * sum |d ln det / d ln v| over the per-layer cosh/sinh
+    values and square roots, checked against the same sum from 40-digit finite differences,
+    at an ill-conditioned point (long lambda, low c: D ~ 1e-6 by cancellation) and a benign one."""
+    import mpmath as mp
+
+    w = synth.workload("ensemble", M=400)
+    m = w.models
+    for mi, lam, c in [(374, 36.38995596158663, 27.531635247710145), (3, 5.0, 150.0)]:
+        a = (m.h[mi], m.alpha[mi], m.beta[mi], m.rho[mi])
+        cp = orc.perturb_velocity(a[1], a[2], c)
+        N = len(a[0])
+        eps = mp.mpf(2) ** -60
+        d0 = _mp_det_pert(*a, lam, cp, -1, -1, eps)
+        tot = 0
+        for pe in range(N + 1):
+            for pw in (range(4, 6) if pe == N else range(6)):
+                d1 = _mp_det_pert(*a, lam, cp, pe, pw, eps)
+                tot += abs(d1 / d0 - 1) / eps
+        want = float(tot) * 2.0 ** -53
+        got = orc.det_kappa(*a, lam, c)
+        assert abs(got - want) <= 0.02 * want, (mi, got, want)
+    assert orc.det_kappa(*(m.h[374], m.alpha[374], m.beta[374], m.rho[374]),
+                         36.38995596158663, 27.531635247710145) > 1e-9
+
+
 def test_P9_extended_grid_matches_pointwise(orc):
     w = synth.workload("tiny")
     m = w.models
