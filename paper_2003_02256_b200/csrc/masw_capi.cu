@@ -100,6 +100,26 @@ Exec resolve(const masw_exec *ex)
     return r;
 }
 
+// The stream-ordered allocator's default pool releases memory back to the OS at every
+// synchronisation (release threshold 0), so the host path's staging buffers (~70 MB for C5)
+// were unmapped and re-mapped on every call; measured on the GPU box as 2-350 ms per call.
+// Keep freed memory in the pool (once per device).
+std::atomic<unsigned long long> g_pool_configured{0};
+
+void configure_pool(int dev)
+{
+    if (dev < 0 || dev >= 64) return;
+    const unsigned long long bit = 1ull << dev;
+    if (g_pool_configured.load(std::memory_order_acquire) & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    g_pool_configured.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 // Restores the caller's current device on scope exit.
 struct DeviceScope {
     int prev = -1;
@@ -111,6 +131,7 @@ struct DeviceScope {
             CK(cudaSetDevice(dev));
             changed = true;
         }
+        configure_pool(dev >= 0 ? dev : prev);
     }
     ~DeviceScope()
     {
