@@ -364,7 +364,7 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
     // Minimise tail idle (~ resident_warps / (2 TEAM rows)) + speculation waste
     // (~ 16 TEAM / dets_per_row) with dets_per_row ~ V/2:  TEAM* = sqrt(Wres d / (32 R)).
     const int sms = sm_count(device);
-    const double wres = sms * 32.0;
+    const double wres = sms * 24.0;   // resident warps: 3 CTAs x 8 warps per SM (launch bounds)
     const double d = (double)V / 2.0;
     const double t = sqrt(wres * d / (32.0 * (double)(rows > 0 ? rows : 1)));
     int team = 1;
