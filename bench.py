@@ -408,7 +408,7 @@ def run_ours(args):
     }
     if not args.no_extra and world == 1:
         line["other_configs"] = other_configs(masw, torch, dev)
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:   # the oracle baseline runs at N = 1 only
         cores = host_cores()
         n, d, s = oracle_sample(mods, w.lam, w.c, w.ce, args.cpu_seconds, cores)
         line["cpu_baseline"] = {"value": d / s, "unit": UNIT, "cores": cores, "kind": "oracle",

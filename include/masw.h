@@ -93,6 +93,14 @@ typedef struct {
 /* exec.flags */
 #define MASW_ASYNC 0x1u       /* device pointers: no status readback, return after enqueue  */
 #define MASW_TIME_SCAN 0x2u   /* record CUDA events around the scan kernel (masw_last_scan_ms) */
+/* Row schedule of the scan (default: a work-stealing queue over rows, lambda-major).  The two
+ * static schedules are the paper's partitions, here over the kernel's teams:
+ * team g of G takes a contiguous block of rows, or rows g, g+G, g+2G, ... (load-balance
+ * study; results are identical for every schedule). */
+#define MASW_SCHED_CONTIGUOUS 0x4u
+#define MASW_SCHED_MODULAR 0x8u
+/* record each team's algorithmic det count (masw_last_team_dets; synchronous calls only) */
+#define MASW_TEAM_STATS 0x10u
 
 /* Execution options; a NULL masw_exec means {device = current, stream = legacy default,
  * team_warps = 0 (auto), flags = 0}. */
@@ -164,6 +172,11 @@ double masw_last_scan_ms(void);
  * the last 64), oldest first, into ms_out[0..n); waits for their end events.  Returns the
  * number written (<= n) or MASW_E_ARG. */
 int masw_recent_scan_ms(double *ms_out, int32_t n);
+
+/* Per-team algorithmic det counts (sum of idx+1 over the rows each team scanned) of the
+ * calling thread's last synchronous call made with MASW_TEAM_STATS, into out[0..n).  Returns
+ * the number of teams of that launch (which may exceed n), or -1 if none was recorded. */
+int64_t masw_last_team_dets(int64_t *out, int64_t n);
 
 /* Algorithmic work of the calling thread's last curve/ensemble call: the early-exit
  * determinant count sum_rows (idx+1) of SPEC.md:246 (rows with idx < 0 count V for -1 and

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "../../include/masw.h"
 #include "masw_det.cuh"
@@ -28,6 +29,8 @@ constexpr int kScanRing = 64;
 thread_local cudaEvent_t t_scan_ev[kScanRing][2] = {};
 thread_local long long t_scan_count = 0;   // TIME_SCAN launches recorded by this thread
 thread_local long long t_last_alg = -1, t_last_eval = -1;
+thread_local std::vector<long long> t_team_dets;
+thread_local long long t_team_count = -1;
 
 struct Fail {
     int code;
@@ -260,7 +263,16 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         CK(launch_validate(mod, dlam, L, dc, V, dce, ws, st));
 
         const int team = ex.team ? ex.team : auto_team_warps(R, V, dev);
-        ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws, dce ? 0x7Fu : 0x1Fu};
+        const int sched = (ex.flags & MASW_SCHED_CONTIGUOUS) ? 1 : ((ex.flags & MASW_SCHED_MODULAR) ? 2 : 0);
+        ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws, dce ? 0x7Fu : 0x1Fu, sched, nullptr};
+        const bool stats = (ex.flags & MASW_TEAM_STATS) != 0 && !(ex.flags & MASW_ASYNC);
+        long long nteams = 0;
+        if (stats) {
+            nteams = scan_teams(sa, team, dev);
+            if (nteams <= 0) return MASW_E_CUDA;
+            sa.team_dets = arena.alloc<unsigned long long>((size_t)nteams);
+            CK(cudaMemsetAsync(sa.team_dets, 0, nteams * sizeof(unsigned long long), st));
+        }
         const bool timed = (ex.flags & MASW_TIME_SCAN) != 0;
         cudaEvent_t *slot = t_scan_ev[t_scan_count % kScanRing];
         if (timed) {
@@ -281,6 +293,12 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         if (code < 0) return code;
         t_last_alg = (long long)w.alg_dets;
         t_last_eval = (long long)w.eval_dets;
+        if (stats) {
+            t_team_dets.assign((size_t)nteams, 0);
+            CK(cudaMemcpy(t_team_dets.data(), sa.team_dets, nteams * sizeof(long long),
+                          cudaMemcpyDeviceToHost));
+            t_team_count = nteams;
+        }
         if (host) {
             CK(cudaMemcpyAsync(ct_out, dct, R * sizeof(double), cudaMemcpyDeviceToHost, st));
             if (idx_out)
@@ -520,6 +538,14 @@ double masw_last_scan_ms(void)
 {
     double ms = -1.0;
     return masw_recent_scan_ms(&ms, 1) == 1 ? ms : -1.0;
+}
+
+int64_t masw_last_team_dets(int64_t *out, int64_t n)
+{
+    if (t_team_count < 0) return -1;
+    if (out)
+        for (int64_t i = 0; i < n && i < t_team_count; ++i) out[i] = t_team_dets[(size_t)i];
+    return t_team_count;
 }
 
 int masw_last_work(int64_t *algorithmic_dets, int64_t *evaluated_dets)

@@ -43,12 +43,17 @@ struct ScanArgs {
     int32_t *idx;      // [M][L] or nullptr
     Workspace *ws;
     unsigned grid_mask;  // Workspace::grid_err bits that invalidate the call (0x1F, 0x7F with C_e)
+    int sched;           // 0 work-stealing queue, 1 static contiguous, 2 static modular
+    unsigned long long *team_dets;  // per-team algorithmic det counts (nullable)
 };
 
 // Launchers (masw_kernels.cu).  Each returns the cudaError_t of its launch.
 cudaError_t launch_validate(const ModelArgs &m, const double *lam, int64_t L, const double *c,
                             int64_t V, const double *ce, Workspace *ws, cudaStream_t st);
-cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device);
+// *teams_out (nullable) receives the number of teams the launch used.
+cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device,
+                        long long *teams_out = nullptr);
+long long scan_teams(const ScanArgs &a, int team_warps, int device);
 cudaError_t launch_misfit(const double *ct, const double *ce, int64_t M, int64_t L,
                           double *misfit, Workspace *ws, unsigned grid_mask, bool check_models,
                           cudaStream_t st);

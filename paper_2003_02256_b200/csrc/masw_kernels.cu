@@ -219,15 +219,31 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     const int64_t M = a.mod.M, L = a.L, V = a.V;
     const int64_t rows = M * L;
     const double *__restrict__ cg = a.c;
-    unsigned long long my_alg = 0, my_eval = 0;
+    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0;
     unsigned my_status = 0;
     int buf = 0;
+    // static schedules (the paper's partitions): team g of G takes a
+    // contiguous block of rows, or rows g, g+G, g+2G, ...
+    const long long G = (long long)gridDim.x * TEAMS;
+    const long long g = (long long)blockIdx.x * TEAMS + team;
+    const long long cbase = rows / G, cextra = rows % G;
+    const long long clo = g * cbase + (g < cextra ? g : cextra);
+    const long long chi = clo + cbase + (g < cextra ? 1 : 0);
+    long long kth = 0;
 
     for (;;) {
-        // ---- pop a row (work-stealing queue; rows i-major so long wavelengths go first
-        //      when lambda is given in the usual decreasing order)
+        // ---- next row: work-stealing queue (default; rows i-major so long wavelengths go
+        //      first when lambda is given in the usual decreasing order) or a
+        //      static schedule
         long long row;
-        if constexpr (TEAM == 1) {
+        if (a.sched == 1) {
+            row = clo + kth;
+            if (row >= chi) row = rows;
+            ++kth;
+        } else if (a.sched == 2) {
+            row = g + kth * G;
+            ++kth;
+        } else if constexpr (TEAM == 1) {
             if (lane == 0) row = (long long)atomicAdd(&ws->queue, 1ull);
             row = __shfl_sync(FULL, row, 0);
         } else {
@@ -319,18 +335,23 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
                     }
                     my_alg += (unsigned long long)(j + 1);
                 }
+                team_alg += (unsigned long long)(first + 1);
                 found = true;
                 break;
             }
         }
-        if (!found && tl == 0) {
-            const int64_t o = m * L + i;
-            a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
-            if (a.idx) a.idx[o] = -1;
-            my_status |= 1u;
-            my_alg += (unsigned long long)V;
+        if (!found) {
+            team_alg += (unsigned long long)V;
+            if (tl == 0) {
+                const int64_t o = m * L + i;
+                a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+                if (a.idx) a.idx[o] = -1;
+                my_status |= 1u;
+                my_alg += (unsigned long long)V;
+            }
         }
     }
+    if (a.team_dets && tl == 0) a.team_dets[g] = team_alg;
 
     // ---- per-warp aggregation of the work counters (one atomic per warp)
     my_alg = warp_sum_u64(my_alg);
@@ -373,7 +394,8 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
 }
 
 template <int TEAM, int BLOCK, int NFIX>
-static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
+static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
+                                 long long *teams_out, bool dry = false)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     const size_t smem = round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
@@ -405,6 +427,8 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
     const int64_t need = (rows + TEAMS - 1) / TEAMS;
     if (need < blocks) blocks = need;
     if (blocks < 1) blocks = 1;
+    if (teams_out) *teams_out = blocks * TEAMS;
+    if (dry) return cudaSuccess;
     kern<<<(unsigned)blocks, BLOCK, smem, st>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -415,16 +439,30 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device)
 //    kernel grew to 9.4k instructions; instruction-cache bound);
 //  * a row-pair kernel sharing the (model, c) terms of two wavelengths per lane: 132 ms
 //    (register-bound: 128 registers with spills, or 230 registers at 8 warps/SM).
-cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device)
+static cudaError_t dispatch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device,
+                                 long long *teams_out, bool dry)
 {
     switch (team_warps) {
-        case 1: return launch_scan_t<1, 256, 0>(a, st, device);
-        case 2: return launch_scan_t<2, 256, 0>(a, st, device);
-        case 4: return launch_scan_t<4, 256, 0>(a, st, device);
-        case 8: return launch_scan_t<8, 256, 0>(a, st, device);
-        case 16: return launch_scan_t<16, 512, 0>(a, st, device);
+        case 1: return launch_scan_t<1, 256, 0>(a, st, device, teams_out, dry);
+        case 2: return launch_scan_t<2, 256, 0>(a, st, device, teams_out, dry);
+        case 4: return launch_scan_t<4, 256, 0>(a, st, device, teams_out, dry);
+        case 8: return launch_scan_t<8, 256, 0>(a, st, device, teams_out, dry);
+        case 16: return launch_scan_t<16, 512, 0>(a, st, device, teams_out, dry);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device,
+                        long long *teams_out)
+{
+    return dispatch_scan(a, team_warps, st, device, teams_out, false);
+}
+
+long long scan_teams(const ScanArgs &a, int team_warps, int device)
+{
+    long long t = 0;
+    if (dispatch_scan(a, team_warps, nullptr, device, &t, true) != cudaSuccess) return -1;
+    return t;
 }
 
 // ------------------------------------------------------------------ misfit (Algorithm 2)

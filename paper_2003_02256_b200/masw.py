@@ -22,6 +22,7 @@ OK, WARN_NO_SIGN_CHANGE = 0, 1
 E_ARG, E_MODEL, E_GRID, E_RANGE, E_NONFINITE, E_CUDA, E_NOMEM = -1, -2, -3, -4, -5, -6, -7
 IDX_NO_CHANGE, IDX_NONFINITE = -1, -2
 ASYNC, TIME_SCAN = 0x1, 0x2
+SCHED_CONTIGUOUS, SCHED_MODULAR, TEAM_STATS = 0x4, 0x8, 0x10
 MAX_LAYERS = 64
 
 
@@ -77,6 +78,8 @@ def lib():
         L.masw_last_cuda_error.restype = ctypes.c_char_p
         L.masw_kernel_launches.restype = ctypes.c_int64
         L.masw_last_scan_ms.restype = ctypes.c_double
+        L.masw_last_team_dets.restype = ctypes.c_int64
+        L.masw_last_team_dets.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]
         L.masw_recent_scan_ms.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int32]
         L.masw_last_work.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
         L.masw_probe_fp64_peak.argtypes = [ctypes.c_int32, ctypes.c_double,
@@ -271,6 +274,16 @@ def masw_recent_scan_ms(n: int):
     buf = (ctypes.c_double * max(n, 1))()
     k = lib().masw_recent_scan_ms(buf, n)
     return [buf[i] for i in range(max(k, 0))]
+
+
+def masw_last_team_dets():
+    """Per-team algorithmic det counts of the last MASW_TEAM_STATS call (numpy int64)."""
+    n = int(lib().masw_last_team_dets(None, 0))
+    if n < 0:
+        return None
+    out = np.zeros(n, dtype=np.int64)
+    lib().masw_last_team_dets(out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n)
+    return out
 
 
 def masw_last_work():

@@ -362,3 +362,21 @@ def test_async_scan_timing_ring(masw):
                                   flags=masw.ASYNC | masw.TIME_SCAN)
     ms = masw.masw_recent_scan_ms(3)
     assert len(ms) == 3 and all(x > 0 for x in ms)
+
+
+@pytest.mark.parametrize("team", [1, 4])
+def test_static_schedules_same_results_and_team_counts(masw, team):
+    """The paper's static partitions as scan schedules: identical C_t, and the
+    per-team det counts add up to the algorithmic total."""
+    w = synth.workload("ensemble", M=500)
+    m = w.models
+    args = (m.h, m.alpha, m.beta, m.rho, w.lam, w.c, w.ce)
+    ref = masw.masw_curves_ensemble(*args, team_warps=team, flags=masw.TEAM_STATS)
+    alg_ref, _ = masw.masw_last_work()
+    tq = masw.masw_last_team_dets()
+    assert tq is not None and int(tq.sum()) == alg_ref
+    for fl in (masw.SCHED_CONTIGUOUS, masw.SCHED_MODULAR):
+        r = masw.masw_curves_ensemble(*args, team_warps=team, flags=fl | masw.TEAM_STATS)
+        assert np.array_equal(r.idx, ref.idx) and np.array_equal(r.misfit, ref.misfit)
+        t = masw.masw_last_team_dets()
+        assert int(t.sum()) == alg_ref and len(t) == len(tq)

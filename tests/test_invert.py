@@ -1,0 +1,91 @@
+"""Inversion driver: file formats and the search loop.  The per-rank
+compute is the CUDA library on a GPU box (-m gpu) and the injected oracle on CPU."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_2003_02256_b200 import invert as inv
+
+
+def test_curve_roundtrip_and_grid(tmp_path):
+    lam = synth.variable_lambdas()
+    ce = synth.load_golden("c2_ct_oracle.txt")
+    p = tmp_path / "ce.csv"
+    inv.write_curve(str(p), lam, ce)
+    l2, c2 = inv.read_curve(str(p))
+    assert np.array_equal(l2, lam) and np.array_equal(c2, ce)       # byte-for-value
+    g = inv.parse_grid("0.5:500:0.5")
+    assert np.array_equal(g, synth.maswaves_grid())
+    assert np.array_equal(inv.parse_grid("100:350:100"), [100.0, 200.0, 300.0])
+    with pytest.raises(ValueError):
+        inv.parse_grid("50:50.5:1")                                                     # < 2 points
+
+
+def _bounds():
+    return inv.Bounds({"h": [[0.5, 1.5], [0.5, 1.5], [1, 3], [1, 3], [2, 6]],
+                       "beta": [[60, 90], [70, 110], [120, 180], [150, 210], [200, 280],
+                                [250, 330]],
+                       "alpha_over_beta": [4.0, 6.0], "rho": [[1700, 2000]] * 6})
+
+
+def test_bounds_draw_valid_and_prefix_stable():
+    import oracle
+
+    b = _bounds()
+    x = b.draw(np.random.Generator(np.random.PCG64(3)), 500)
+    y = b.draw(np.random.Generator(np.random.PCG64(3)), 200)
+    assert all(np.array_equal(u[:200], v) for u, v in zip(x, y))
+    h, a, be, r = x
+    for m in range(0, 500, 37):
+        assert oracle.validate_model(h[m], a[m], be[m], r[m]) == 0
+
+
+def test_invert_with_oracle_ops_finds_generating_model():
+    """A batch containing the model that generated C_e: misfit 0, ranked first."""
+    import oracle
+    from test_distributed_cpu import oracle_ops
+
+    b = _bounds()
+    truth = b.draw(np.random.Generator(np.random.PCG64(11)), 1)
+    lam = synth.variable_lambdas()[::4]
+    c = synth.maswaves_grid()
+    st, ce, idx, nd = oracle.curve(truth[0][0], truth[1][0], truth[2][0], truth[3][0], lam, c)
+    assert st == 0
+
+    class Seeded(inv.Bounds):
+        def draw(self, rng, M):
+            h, a, be, r = b.draw(rng, M)
+            k = 5
+            h[k], a[k], be[k], r[k] = truth[0][0], truth[1][0], truth[2][0], truth[3][0]
+            return h, a, be, r
+
+    sb = Seeded.__new__(Seeded)
+    sb.__dict__.update(b.__dict__)
+    best, n = inv.invert(lam, ce, c, sb, n_models=24, batch=12, seed=1, top=3,
+                         device=torch.device("cpu"), ops=oracle_ops())
+    assert n == 24 and best[0][0] == 0.0 and best[0][1] == 5
+    assert best[0][0] <= best[1][0] <= best[2][0]
+
+
+@pytest.mark.gpu
+def test_invert_cli_on_gpu(tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    w = synth.workload("maswaves")
+    p = tmp_path / "ce.csv"
+    inv.write_curve(str(p), w.lam, w.ce)
+    bj = tmp_path / "b.json"
+    json.dump({"h": [[0.8, 1.2], [0.8, 1.2], [1.5, 2.5], [1.5, 2.5], [3, 5]],
+               "beta": [[70, 80], [85, 95], [140, 160], [170, 190], [230, 250], [280, 300]],
+               "alpha": [[1440, 1440]] * 6, "rho": [[1850, 1850]] * 6}, open(bj, "w"))
+    out = tmp_path / "best.csv"
+    assert inv.main(["--curve", str(p), "--bounds", str(bj), "--models", "3000", "--batch",
+                     "1000", "--top", "5", "--out", str(out)]) == 0
+    rows = open(out).read().strip().splitlines()
+    assert len(rows) == 6
+    best = float(rows[1].split(",")[2])
+    assert best < 0.05                       # the C2 model lies inside these bounds
