@@ -118,14 +118,13 @@ __device__ __forceinline__ double rsqrt_fast(double q)
     return fma(h, e, y);
 }
 
-// sqrt(q) and 1/sqrt(q) for finite q > 0: the refined reciprocal root plus one
-// residual correction of the root (x = x0 + (q - x0^2) / (2 x0)), ~0.5 ulp like IEEE sqrt.
+// sqrt(q) and 1/sqrt(q) for finite q > 0: x = q * (1/sqrt q) (~1.5 ulp).  No residual
+// correction: det K is ~1e4 times less sensitive to 1-ulp errors in the square roots r, s
+// than to errors in the cosh values (kappa analysis, reading S15'), measured per term.
 __device__ __forceinline__ void sqrt_rsqrt(double q, double &x, double &rx)
 {
     rx = rsqrt_fast(q);
-    const double x0 = q * rx;
-    const double res = fma(-x0, x0, q);
-    x = fma(0.5 * rx, res, x0);
+    x = q * rx;
 }
 
 // x * 2^k by exponent arithmetic (no overflow/underflow for the ranges used here).
