@@ -13,6 +13,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/masw.h"
 #include "masw_det.cuh"
 #include "masw_internal.h"
@@ -353,6 +355,12 @@ int run_misfit(const double *ct, const double *ce, int64_t M, int64_t L, double 
     }
 }
 
+// NVTX range around each C-ABI call (header-only NVTX v3; a no-op unless a tool attaches).
+struct Range {
+    explicit Range(const char *name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
+
 }  // namespace
 
 // ====================================================================== extern "C"
@@ -361,6 +369,7 @@ extern "C" {
 int masw_curve(const masw_model *model, const double *lambda, int64_t L, const double *c,
                int64_t V, double *ct_out, int32_t *idx_out, const masw_exec *exec)
 {
+    Range nvtx_range("masw_curve");
     if (!model) return MASW_E_ARG;
     ModelArgs m{1, model->n_layers, model->h, model->alpha, model->beta, model->rho};
     return run_curves(m, lambda, L, c, V, nullptr, ct_out, idx_out, nullptr, exec);
@@ -370,6 +379,7 @@ int masw_curves_ensemble(const masw_ensemble *ens, const double *lambda, int64_t
                          const double *c, int64_t V, const double *ce, double *ct_out,
                          int32_t *idx_out, double *misfit_out, const masw_exec *exec)
 {
+    Range nvtx_range("masw_curves_ensemble");
     if (!ens) return MASW_E_ARG;
     ModelArgs m{ens->n_models, ens->n_layers, ens->h, ens->alpha, ens->beta, ens->rho};
     return run_curves(m, lambda, L, c, V, ce, ct_out, idx_out, misfit_out, exec);
@@ -378,18 +388,21 @@ int masw_curves_ensemble(const masw_ensemble *ens, const double *lambda, int64_t
 int masw_misfit(const double *ct, const double *ce, int64_t L, double *misfit_out,
                 const masw_exec *exec)
 {
+    Range nvtx_range("masw_misfit");
     return run_misfit(ct, ce, 1, L, misfit_out, exec);
 }
 
 int masw_misfit_batch(const double *ct, const double *ce, int64_t M, int64_t L,
                       double *misfit_out, const masw_exec *exec)
 {
+    Range nvtx_range("masw_misfit_batch");
     return run_misfit(ct, ce, M, L, misfit_out, exec);
 }
 
 int masw_argmin(const double *misfit, int64_t M, int64_t *best_out, double *best_misfit_out,
                 const masw_exec *exp)
 {
+    Range nvtx_range("masw_argmin");
     if (!misfit || !best_out || M < 0) return MASW_E_ARG;
     if (M == 0) {
         int d = -1;
@@ -439,6 +452,7 @@ int masw_det_grid(const masw_model *model, const double *lambda, int64_t L, cons
                   int64_t V, double *mant_re, double *mant_im, int32_t *exp2,
                   const masw_exec *exp)
 {
+    Range nvtx_range("masw_det_grid");
     if (!model || !model->h || !model->alpha || !model->beta || !model->rho || !lambda || !c ||
         !mant_re || !mant_im || !exp2)
         return MASW_E_ARG;

@@ -29,6 +29,10 @@
 
 #include <cstdint>
 
+#ifndef MASW_LAYER_UNROLL
+#define MASW_LAYER_UNROLL 1
+#endif
+
 namespace masw {
 
 constexpr double kTwoPi = 6.283185307179586;   // reading S2 / O1
@@ -533,7 +537,8 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
 #pragma unroll
         for (int t = 0; t + 1 < NFIX; ++t) node_step(t);
     } else {
-#pragma unroll 1
+        constexpr int kLayerUnroll = MASW_LAYER_UNROLL;
+#pragma unroll kLayerUnroll
         for (int t = 0; t + 1 < N; ++t) node_step(t);
     }
 

@@ -178,11 +178,13 @@ __host__ __device__ inline unsigned team_model_bytes(int N)
                    2u * (unsigned)(N + 1) * (unsigned)sizeof(double));
 }
 
-// Resident CTAs per SM requested from ptxas: 768 threads/SM (3 x 256 -> <= 85 registers;
-// measured on B200: +5% over the unconstrained 94-register build despite ~60 B of L1-resident
-// spills).  -DMASW_SCAN_MINB=k overrides it for 256-thread CTAs (0 = unconstrained).
+// Resident CTAs per SM requested from ptxas for 256-thread CTAs: 2 (<= 128 registers; the
+// kernel needs 122 without spills).  Measured on B200 with the current kernel: equal to the
+// 3-CTA / 80-register build on C5 and ~5% faster on C3/C4 (the 3-CTA build spills ~100 B;
+// it was the better choice before the elementary functions were trimmed).
+// -DMASW_SCAN_MINB=k overrides it (0 = unconstrained).
 #ifndef MASW_SCAN_MINB
-#define MASW_SCAN_MINB 3
+#define MASW_SCAN_MINB 2
 #endif
 template <int BLOCK>
 constexpr int scan_min_blocks()
@@ -385,9 +387,11 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
     // Minimise tail idle (~ resident_warps / (2 TEAM rows)) + speculation waste
     // (~ 16 TEAM / dets_per_row) with dets_per_row ~ V/2:  TEAM* = sqrt(Wres d / (32 R)).
     const int sms = sm_count(device);
-    const double wres = sms * 24.0;   // resident warps: 3 CTAs x 8 warps per SM (launch bounds)
+    const double wres = sms * 16.0;   // resident warps: 2 CTAs x 8 warps per SM (launch bounds)
     const double d = (double)V / 2.0;
-    const double t = sqrt(wres * d / (32.0 * (double)(rows > 0 ? rows : 1)));
+    // halved: measured team optima on C3/C4 (1-2) sit below the bare tail/waste model (4),
+    // which ignores the per-chunk team barriers
+    const double t = 0.5 * sqrt(wres * d / (32.0 * (double)(rows > 0 ? rows : 1)));
     int team = 1;
     while (team * 2 <= t && team < 16) team *= 2;
     return team;

@@ -380,3 +380,24 @@ def test_static_schedules_same_results_and_team_counts(masw, team):
         assert np.array_equal(r.idx, ref.idx) and np.array_equal(r.misfit, ref.misfit)
         t = masw.masw_last_team_dets()
         assert int(t.sum()) == alg_ref and len(t) == len(tq)
+
+
+def test_sharded_drivers_with_cuda_ops(masw, orc):
+    """distributed.curve_sharded / ensemble_sharded with the CUDA library as per-rank compute
+    (world size 1 here; N > 1 host logic is covered by tests/test_distributed_cpu.py)."""
+    from paper_2003_02256_b200 import distributed as D
+
+    w = synth.workload("maswaves")
+    m = w.models
+    model = tuple(dev(x[0]) for x in (m.h, m.alpha, m.beta, m.rho))
+    for strat in ("modular", "contiguous"):
+        out = D.curve_sharded(model, dev(w.lam), dev(w.c), dev(w.ce), strategy=strat)
+        ost, oct_, oidx, _ = orc.curve(*margs(m), w.lam, w.c)
+        assert np.array_equal(out.idx.cpu().numpy(), oidx)
+        assert parity.misfit_ok(orc, out.ct.cpu().numpy(), w.ce, out.misfit)
+    e = synth.workload("ensemble", M=64)
+    em = e.models
+    res = D.ensemble_sharded(tuple(dev(x) for x in (em.h, em.alpha, em.beta, em.rho)),
+                             dev(e.lam), dev(e.c), dev(e.ce))
+    o = orc.ensemble(em, e.lam, e.c, e.ce)
+    assert np.array_equal(res.idx.cpu().numpy(), o["idx"]) and res.best == o["best"]
