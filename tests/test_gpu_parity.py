@@ -288,7 +288,7 @@ def test_ensemble_full_size_sampled(masw, orc):
     mis = res.misfit.cpu().numpy()
     assert res.status in (0, 1)
     rng = np.random.default_rng(200302256)
-    sample = np.unique(np.r_[rng.choice(100_000, 150, replace=False), np.argsort(mis)[:20],
+    sample = np.unique(np.r_[rng.choice(100_000, 600, replace=False), np.argsort(mis)[:20],
                              [0, 99_999]])
     sub = mods.take(sample)
     o = orc.ensemble(sub, w.lam, w.c, w.ce)
