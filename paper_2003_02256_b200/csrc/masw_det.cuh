@@ -98,28 +98,28 @@ constexpr double kPio2_1 = 1.57079632673412561417e+00;  // pi/2 split in 33+33+5
 constexpr double kPio2_2 = 6.07710050650619224932e-11;  // (exact n*pio2_1 for n < 2^20)
 constexpr double kPio2_3 = 2.02226624879595063154e-21;
 
-// 1/x for finite normal x: MUFU approximation + two Newton steps (0 -> NaN, caught as bad).
+// The MUFU fp64 seeds (rcp.approx.ftz.f64, rsqrt.approx.ftz.f64) have relative error
+// e <= 2^-20.1 on sm_100a (scripts/mufu_accuracy.cu, measured on B200), so ONE higher-order
+// correction reaches full precision: its truncation error is O(e^3) ~ 2^-60.
+
+// 1/x for finite normal x: y0 (1 + e + e^2), e = 1 - x y0 (max 0.999 * 2^-53 relative,
+// measured; the same as two Newton steps, one DFMA fewer).  0 -> NaN (callers guard).
 __device__ __forceinline__ double rcp_fast(double x)
 {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-x, y, 1.0);
-    return fma(y, e, y);
+    const double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
 }
 
-// 1/sqrt(q) for finite q > 0: MUFU approximation + two Newton steps.
+// 1/sqrt(q) for finite q > 0: y0 (1 + e/2 + 3e^2/8), e = 1 - q y0^2 (max 1.005 * 2^-53
+// relative, measured; two Newton steps give 1.24 * 2^-53 in eight FP64 ops, this five).
 __device__ __forceinline__ double rsqrt_fast(double q)
 {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
-    double h = 0.5 * y;
-    double e = fma(-q * y, y, 1.0);
-    y = fma(h, e, y);
-    h = 0.5 * y;
-    e = fma(-q * y, y, 1.0);
-    return fma(h, e, y);
+    const double e = fma(-q * y, y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
 }
 
 // sqrt(q) and 1/sqrt(q) for finite q > 0: x = q * (1/sqrt q) (~1.5 ulp).  No residual
@@ -293,20 +293,23 @@ __device__ __forceinline__ double perturb_velocity(const double *__restrict__ ve
 //   k22 = f (SXr Cs - Cr XSs)    k24 = f (XSs - SXr)
 // Element layout (DOFs u_top, w_top, u_bot, w_bot):
 //   [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12], [k14, k24, -k12, k22]]
+// Evaluation: Cr Cs - 1 is one fused op (exact product, one rounding; it is -(1 - Cr Cs) in
+// both D and k12), and mu (1 + s^2) = k rho (2 beta^2 - c^2) = 2 mu - k rho c^2 reuses k rho c^2.
 struct Elem {
     double k11, k12, k13, k14, k22, k24;
 };
 
 __device__ __forceinline__ Elem elem_from_triples(double Cr, double XSr, double SXr, double Cs,
                                                   double XSs, double SXs, double krho, double mu,
-                                                  double c2, double qb)
+                                                  double c2)
 {
-    const double CC = Cr * Cs;
-    const double D = fma(SXr, SXs, fma(XSr, XSs, 2.0 * (1.0 - CC)));
-    const double f = (krho * c2) * rcp_fast(D);
+    const double cm1 = fma(Cr, Cs, -1.0);                              // Cr Cs - 1
+    const double D = fma(XSr, XSs, fma(-2.0, cm1, SXr * SXs));
+    const double kc2 = krho * c2;
+    const double f = kc2 * rcp_fast(D);
     Elem E;
     E.k11 = f * fma(Cr, SXs, -XSr * Cs);
-    E.k12 = fma(f, fma(-XSr, XSs, CC - 1.0), -mu * (1.0 + qb));
+    E.k12 = fma(f, fma(-XSr, XSs, cm1), fma(-2.0, mu, kc2));
     E.k13 = f * (XSr - SXs);
     E.k14 = f * (Cs - Cr);
     E.k22 = f * fma(SXr, Cs, -Cr * XSs);
@@ -343,7 +346,7 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
         Cr = t[0]; XSr = t[1]; SXr = t[2];
         Cs = t[3]; XSs = t[4]; SXs = t[5];
     }
-    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2, qb);
+    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2);
 }
 
 // -------------------------------------------------------------- determinant
@@ -383,13 +386,26 @@ struct DetOut {
 // trailing complex columns (2 in the last step, whose node-N columns carry K_hs).
 struct StepOut {
     double piv0, piv1;
-    int parity;   // parity of the two GEPP row swaps
+    int key0, key1;   // mag_key of the two pivots (0 <=> zero pivot, >= 0x7ff00000 <=> Inf/NaN)
+    int parity;       // parity of the two GEPP row swaps
 };
 
 // |x| ordering key: the high word without the sign bit (exponent + top 20 mantissa bits).
 // Comparing keys picks a pivot within 2^-20 of the largest magnitude -- as stable as exact
 // partial pivoting -- with one integer op per candidate instead of an FP64-pipe DSETP.
 __device__ __forceinline__ int mag_key(double x) { return __double2hiint(x) & 0x7fffffff; }
+
+// Entries known to be ZERO at compile time, so their updates are skipped (fma(-l, 0, x) is
+// x for finite l; a non-finite l already poisons the row's other columns, so the Inf/NaN
+// bookkeeping is unchanged).  Before the step, rows 0, 1 (left over from node t-1) are zero
+// in node t+2's columns (c >= 4 when NC = 6) and have no imaginary part; rows 2, 3 are
+// imaginary only in the trailing NR columns.  After column 0 is eliminated with pivot row P,
+// row i keeps a zero iff it and row P both had one.  With P in {0, 1} (3/4 of the steps on
+// C5) this removes 6-10 of the step's 23 DFMAs.
+template <int NC, int NR>
+__device__ __forceinline__ constexpr bool zre0(int i, int c) { return NC == 6 && i < 2 && c >= 4; }
+template <int NC, int NR>
+__device__ __forceinline__ constexpr bool zim0(int i, int c) { return i < 2 || c < NC - NR; }
 
 template <int NC, int NR, int P, int Q>
 __device__ __forceinline__ void gepp_finish(double (&R)[4][NC], double (&Ri)[4][NC],
@@ -404,18 +420,26 @@ __device__ __forceinline__ void gepp_finish(double (&R)[4][NC], double (&Ri)[4][
     constexpr int lo = (Q == 2) ? pos1 : pos2;
     constexpr int hi = (Q == 3) ? pos1 : pos3;
     o.piv1 = R[prow][1];
-    const double inv1 = (o.piv1 != 0.0) ? rcp_fast(o.piv1) : 0.0;
+    const double inv1 = o.key1 ? rcp_fast(o.piv1) : 0.0;
     const double l_lo = R[lo][1] * inv1, l_hi = R[hi][1] * inv1;
+    // zero pattern after the column-0 elimination (rows != P)
+    constexpr auto zr = [](int i, int c) { return zre0<NC, NR>(i, c) && zre0<NC, NR>(P, c); };
+    constexpr auto zi = [](int i, int c) { return zim0<NC, NR>(i, c) && zim0<NC, NR>(P, c); };
 #pragma unroll
     for (int c = 2; c < NC; ++c) {
-        X[0][c - 2] = fma(-l_lo, R[prow][c], R[lo][c]);
-        X[1][c - 2] = fma(-l_hi, R[prow][c], R[hi][c]);
-        if (c >= NC - NR) {
-            Xi[0][c - 2] = fma(-l_lo, Ri[prow][c], Ri[lo][c]);
-            Xi[1][c - 2] = fma(-l_hi, Ri[prow][c], Ri[hi][c]);
+        if (zr(prow, c)) {
+            X[0][c - 2] = zr(lo, c) ? 0.0 : R[lo][c];
+            X[1][c - 2] = zr(hi, c) ? 0.0 : R[hi][c];
         } else {
-            Xi[0][c - 2] = 0.0;
-            Xi[1][c - 2] = 0.0;
+            X[0][c - 2] = fma(-l_lo, R[prow][c], R[lo][c]);
+            X[1][c - 2] = fma(-l_hi, R[prow][c], R[hi][c]);
+        }
+        if (zi(prow, c)) {
+            Xi[0][c - 2] = zi(lo, c) ? 0.0 : Ri[lo][c];
+            Xi[1][c - 2] = zi(hi, c) ? 0.0 : Ri[hi][c];
+        } else {
+            Xi[0][c - 2] = zi(lo, c) ? -l_lo * Ri[prow][c] : fma(-l_lo, Ri[prow][c], Ri[lo][c]);
+            Xi[1][c - 2] = zi(hi, c) ? -l_hi * Ri[prow][c] : fma(-l_hi, Ri[prow][c], Ri[hi][c]);
         }
     }
     o.parity = (P != 0) ^ (Q != 1);
@@ -427,16 +451,19 @@ __device__ __forceinline__ void gepp_after_p(double (&R)[4][NC], double (&Ri)[4]
                                              double (&Xi)[2][NC - 2])
 {
     o.piv0 = R[P][0];
-    const double inv0 = (o.piv0 != 0.0) ? rcp_fast(o.piv0) : 0.0;
-    // eliminate column 0 from the three other rows with pivot row P
+    const double inv0 = o.key0 ? rcp_fast(o.piv0) : 0.0;
+    // eliminate column 0 from the three other rows with pivot row P (skipping the pivot
+    // row's known zeros)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         if (i == P) continue;
         const double l = R[i][0] * inv0;
 #pragma unroll
         for (int c = 1; c < NC; ++c) {
-            R[i][c] = fma(-l, R[P][c], R[i][c]);
-            if (c >= NC - NR) Ri[i][c] = fma(-l, Ri[P][c], Ri[i][c]);
+            if (!zre0<NC, NR>(P, c))
+                R[i][c] = zre0<NC, NR>(i, c) ? -l * R[P][c] : fma(-l, R[P][c], R[i][c]);
+            if (!zim0<NC, NR>(P, c))
+                Ri[i][c] = zim0<NC, NR>(i, c) ? -l * Ri[P][c] : fma(-l, Ri[P][c], Ri[i][c]);
         }
     }
     // column-1 pivot among positions 1..3 (rows pos1, pos2, pos3), first max wins
@@ -444,6 +471,7 @@ __device__ __forceinline__ void gepp_after_p(double (&R)[4][NC], double (&Ri)[4]
     constexpr int pos2 = (P == 2) ? 0 : 2;
     constexpr int pos3 = (P == 3) ? 0 : 3;
     const int b1 = mag_key(R[pos1][1]), b2 = mag_key(R[pos2][1]), b3 = mag_key(R[pos3][1]);
+    o.key1 = max(b1, max(b2, b3));
     if (b2 > b1 && b2 >= b3) {
         gepp_finish<NC, NR, P, 2>(R, Ri, o, X, Xi);
     } else if (b3 > b1 && b3 > b2) {
@@ -465,6 +493,7 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
     if (a1 > best) { best = a1; p = 1; }
     if (a2 > best) { best = a2; p = 2; }
     if (a3 > best) { best = a3; p = 3; }
+    o.key0 = best;
     switch (p) {
         case 0: gepp_after_p<NC, NR, 0>(R, Ri, o, X, Xi); break;
         case 1: gepp_after_p<NC, NR, 1>(R, Ri, o, X, Xi); break;
@@ -487,8 +516,8 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
 // (reading S3/S5), so the pivots and all but the last node's columns are real fp64; only
 // node N's columns (K_hs) are complex.  det K = (-1)^parity * prod pivots * det(last 2x2).
 // Cost per node: one layer element + one 4-row GEPP step, O(N) in total.
-// `maybe_near` = false asserts that no layer velocity lies within 1e-3 of c (the scan
-// decides it once per warp for its 32 velocities), which skips the per-lane S4 loop exactly.
+// `maybe_near` = false means c is already the S4-perturbed velocity (the scan resolves S4
+// per warp for its 32 velocities, see scan_kernel), which skips the per-lane S4 loop.
 // NFIX > 0 compiles the determinant for exactly NFIX layers (fully unrolled: no loop-carried
 // register copies, constant shared-memory offsets); NFIX = 0 takes N at run time.
 template <bool WANT_VALUE, int NFIX = 0>
@@ -500,9 +529,13 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     const double cp = maybe_near ? perturb_velocity(vel, 2 * (N + 1), c) : c;
     const double c2 = cp * cp;
 
-    int neg = 0, perm = 0;
-    bool zero = false, bad = false;
-    double nf = 0.0;   // NaN once any pivot / the last det is NaN or Inf
+    // Sign, zero and non-finite bookkeeping in integer ops on the pivots' high words (off the
+    // FP64 pipe): sgn accumulates the XOR of the pivots' sign bits; a zero pivot has key 0, an
+    // Inf/NaN pivot a key >= 0x7ff00000 (NaN keys exceed every finite key, so a NaN entry is
+    // always picked as a pivot or reaches the last 2x2 through the updates).
+    int perm = 0;
+    unsigned sgn = 0;
+    int kmin = 0x7fffffff, kmax = 0;
     DetAcc acc{1.0, 0};
 
     Elem P = layer_elem(load_lc(lc), c2);
@@ -518,18 +551,13 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
         double Ri[4][6];   // unused (real step): NR = 0
         double Xi[2][4];
         const StepOut so = gepp_step<6, 0>(R, Ri, X, Xi);
-        const double piv0 = so.piv0, piv1 = so.piv1;
-        // t = piv0 * piv1 carries both signs, is 0 iff a pivot is 0, and is non-finite iff a
-        // pivot is (|pivots| are far from the fp64 range limits); nf turns NaN on the first
-        // non-finite t and stays NaN.
-        const double tp = piv0 * piv1;
-        neg ^= so.parity ^ (tp < 0.0);
+        sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
+        kmin = min(kmin, min(so.key0, so.key1));
+        kmax = max(kmax, max(so.key0, so.key1));
         perm ^= so.parity;
-        zero |= (tp == 0.0);
-        nf = fma(tp, 0.0, nf);
         if (WANT_VALUE) {
-            acc.mul(piv0);
-            acc.mul(piv1);
+            acc.mul(so.piv0);
+            acc.mul(so.piv1);
         }
         P = Q;
     };
@@ -583,25 +611,23 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
                        {0.0, 0.0, h12i, h22i}};
     double Y[2][2], Yi[2][2];
     const StepOut so = gepp_step<4, 2>(R, Ri, Y, Yi);
-    const double piv0 = so.piv0, piv1 = so.piv1;
-    const double tp = piv0 * piv1;
-    neg ^= so.parity ^ (tp < 0.0);
+    sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
+    kmin = min(kmin, min(so.key0, so.key1));
+    kmax = max(kmax, max(so.key0, so.key1));
     perm ^= so.parity;
-    zero |= (tp == 0.0);
-    nf = fma(tp, 0.0, nf);
     if (WANT_VALUE) {
-        acc.mul(piv0);
-        acc.mul(piv1);
+        acc.mul(so.piv0);
+        acc.mul(so.piv1);
     }
     // det of the last complex 2x2
     const double dre = fma(Y[0][0], Y[1][1], -Yi[0][0] * Yi[1][1]) -
                        fma(Y[0][1], Y[1][0], -Yi[0][1] * Yi[1][0]);
     const double dim = fma(Y[0][0], Yi[1][1], Yi[0][0] * Y[1][1]) -
                        fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
-    nf = fma(dre, 0.0, fma(dim, 0.0, nf));
-    bad = !(nf == 0.0);
-    zero |= (dre == 0.0);
-    neg ^= (dre < 0.0);
+    kmax = max(kmax, max(mag_key(dre), mag_key(dim)));
+    const bool bad = kmax >= 0x7ff00000;
+    const bool zero = (kmin == 0) || (dre == 0.0);
+    const bool neg = (perm != 0) ^ ((sgn >> 31) != 0) ^ (dre < 0.0);
 
     DetOut out;
     out.bad = bad;

@@ -280,23 +280,34 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
         bool found = false;
         for (int64_t base = 0; base < V; base += 32 * TEAM) {
             const int64_t j = base + tl;
-            // Is any layer velocity within 1e-3 of this warp's velocity range?  (S4 check
-            // needed only then; the grid is strictly increasing.)
-            bool near = false;
+            // Reading S4 without a per-lane loop over all 2(N+1) layer velocities: the grid is
+            // strictly increasing, so only velocities inside this warp's range [c_lo, c_hi]
+            // (+-1e-3) can be within 1e-4 of a lane's c.  The warp ballots them (usually none,
+            // rarely one or two); a lane tests just those, and only a lane that IS within 1e-4
+            // of one runs the full S4 loop (exact: its perturbed c' may approach any velocity).
+            const int nv = 2 * (N + 1);
+            double c = 0.0;
+            if (j < V) c = cg[j];
             {
                 const int64_t w0 = base + wt * 32;
                 const double clo = cg[min(w0, V - 1)] - 1e-3;
                 const double chi = cg[min(w0 + 31, V - 1)] + 1e-3;
-                for (int e = lane; e < 2 * (N + 1); e += 32) {
-                    const double v = vel[e];
-                    near |= (v > clo) && (v < chi);
+                bool lane_near = false;
+                for (int e0 = 0; e0 < nv; e0 += 32) {
+                    bool in = false;
+                    if (e0 + lane < nv) {
+                        const double v = vel[e0 + lane];
+                        in = (v > clo) && (v < chi);
+                    }
+                    for (unsigned b = __ballot_sync(FULL, in); b; b &= b - 1)
+                        lane_near |= fabs(c - vel[e0 + __ffs(b) - 1]) < kPerturbTol;
                 }
-                near = __any_sync(FULL, near);
+                if (lane_near) c = perturb_velocity(vel, nv, c);
             }
             int s = 0;
             bool bad = false;
             if (j < V) {
-                const DetOut d = det_K<false, NFIX>(lc, vel, N, cg[j], near);
+                const DetOut d = det_K<false, NFIX>(lc, vel, N, c, false);
                 s = d.sign;
                 bad = d.bad;
                 ++my_eval;
