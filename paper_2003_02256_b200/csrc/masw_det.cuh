@@ -90,13 +90,44 @@ static __constant__ double c_cos[7] = {-1.1353379638297575e-11, 2.08755823806639
                                        -0.0013888888888861095, 0.04166666666666645, -0.5};
 
 constexpr double kShifter = 6755399441055744.0;         // 1.5 * 2^52: round-to-integer trick
-constexpr double kLog2e = 1.4426950408889634;
-constexpr double kLn2Hi = 6.93147180369123816490e-01;   // ln 2 split (fdlibm)
-constexpr double kLn2Lo = 1.90821492927058770002e-10;
-constexpr double kTwoOverPi = 6.36619772367581382433e-01;
-constexpr double kPio2_1 = 1.57079632673412561417e+00;  // pi/2 split in 33+33+53 bits
-constexpr double kPio2_2 = 6.07710050650619224932e-11;  // (exact n*pio2_1 for n < 2^20)
-constexpr double kPio2_3 = 2.02226624879595063154e-21;
+// Split constants whose leading part has <= 21 significant bits (low word zero), so the
+// leading part is an instruction immediate (no register materialisation) and n * part is
+// exact for the n that occur; the trailing parts come from the constant bank (c_k).
+constexpr double kLn2Hi = 0.6931471824645996;           // ln 2 = kLn2Hi + c_k[1] (+1.7e-25)
+constexpr double kPio2Hi = 1.570796012878418;           // pi/2 = kPio2Hi + c_k[3] + c_k[4]
+static __constant__ double c_k[6] = {
+    1.4426950408889634,        // 0: log2 e
+    -1.904654299957768e-09,    // 1: ln 2 - kLn2Hi
+    0.6366197723675814,        // 2: 2 / pi
+    3.139164786504813e-07,     // 3: pi/2 - kPio2Hi (53 bits)
+    1.0562999066987428e-23,    // 4: the rest (residual 5e-40)
+    0.375,                     // 5: rsqrt correction coefficient
+};
+
+// 2^(n-1), 2^(-n-1) and their sum and difference (rounded as fp64 addition rounds them) for
+// the cosh/sinh reconstruction, n = 0..511 (th = n ln2 + r <= 350 gives n <= 505): a
+// per-CTA shared-memory table (16 KB) read with two 128-bit loads -- lanes of a warp hold
+// neighbouring velocities, so their n mostly coincide (broadcast).  Filled by
+// exp_scale_fill() at kernel start.
+struct __align__(16) ExpScale {
+    double a, b, apb, amb;
+};
+constexpr int kExpTab = 512;
+static __shared__ ExpScale s_exp_tab[kExpTab];
+
+__device__ __forceinline__ void exp_scale_fill()
+{
+    for (int n = threadIdx.x; n < kExpTab; n += blockDim.x) {
+        const double a = __hiloint2double((n + 1022) << 20, 0);
+        const double b = __hiloint2double((1022 - n) << 20, 0);
+        ExpScale e;
+        e.a = a;
+        e.b = b;
+        e.apb = a + b;
+        e.amb = a - b;
+        s_exp_tab[n] = e;
+    }
+}
 
 // The MUFU fp64 seeds (rcp.approx.ftz.f64, rsqrt.approx.ftz.f64) have relative error
 // e <= 2^-20.1 on sm_100a (scripts/mufu_accuracy.cu, measured on B200), so ONE higher-order
@@ -119,7 +150,7 @@ __device__ __forceinline__ double rsqrt_fast(double q)
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
     const double e = fma(-q * y, y, 1.0);
-    return fma(y * e, fma(e, 0.375, 0.5), y);
+    return fma(y * e, fma(e, c_k[5], 0.5), y);
 }
 
 // sqrt(q) and 1/sqrt(q) for finite q > 0: x = q * (1/sqrt q) (~1.5 ulp).  No residual
@@ -146,11 +177,11 @@ __device__ __forceinline__ double scale2(double x, int k)
 //   sinh = (a - b) + a (E + O) - b (E - O)   (= O exactly structured at n = 0: no cancellation)
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
 {
-    const double t = fma(th, kLog2e, kShifter);
+    const double t = fma(th, c_k[0], kShifter);
     const double nd = t - kShifter;
     const int n = __double2loint(t);
     double r = fma(nd, -kLn2Hi, th);
-    r = fma(nd, -kLn2Lo, r);
+    r = fma(nd, -c_k[1], r);
     const double r2 = r * r;
     double pe = c_expE[0];                     // E / r^2  (~ 1/2! + r^2/4! + ...)
     double po = c_expO[0];                     // O / r    (~ 1 + r^2/3! + ...)
@@ -160,14 +191,14 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
         po = fma(po, r2, c_expO[i]);
     }
     const double E = pe * r2, O = po * r;
-    const double a = __hiloint2double((n + 1022) << 20, 0);    // 2^(n-1)
-    const double b = __hiloint2double((1022 - n) << 20, 0);    // 2^(-n-1)
+    const ExpScale S = s_exp_tab[n & (kExpTab - 1)];
     const double ep = E + O, em = E - O;                       // e^r - 1, e^-r - 1
-    ch = fma(a, ep, fma(b, em, a + b));
-    sh = fma(a, ep, fma(-b, em, a - b));
+    ch = fma(S.a, ep, fma(S.b, em, S.apb));
+    sh = fma(S.a, ep, fma(-S.b, em, S.amb));
 }
 
-// sin and cos of th in [0, 8e5] (< 2^19 pi/2: Cody-Waite reduction exact; near-minimax
+// sin and cos of th in [0, 8e5] (< 2^19 pi/2: 3-part Cody-Waite reduction, the first product
+// exact, each later step one rounding; near-minimax
 // polynomials on |r| <= pi/4: sin to r^13, cos to r^14).  No branches; the caller
 // routes larger arguments to sin_cos_large.
 constexpr double kTrigMax = 8.0e5;
@@ -183,12 +214,12 @@ __device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, dou
 
 __device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
 {
-    const double t = fma(th, kTwoOverPi, kShifter);
+    const double t = fma(th, c_k[2], kShifter);
     const double nd = t - kShifter;
     const int n = __double2loint(t);
-    double r = fma(nd, -kPio2_1, th);
-    r = fma(nd, -kPio2_2, r);
-    r = fma(nd, -kPio2_3, r);
+    double r = fma(nd, -kPio2Hi, th);          // exact (n * kPio2Hi has <= 40 bits)
+    r = fma(nd, -c_k[3], r);
+    r = fma(nd, -c_k[4], r);
     sin_cos_reduced(r, n, sn, cs);
 }
 
@@ -199,7 +230,7 @@ static __device__ __noinline__ void sin_cos_large(double th, double &sn, double 
         sn = cs = __longlong_as_double(0x7ff8000000000000ll);
         return;
     }
-    const double nd = rint(th * kTwoOverPi);
+    const double nd = rint(th * 0.6366197723675814);
     const int n = (int)nd;
     double r = th - nd * kPio2L_1;           // exact (Sterbenz)
     r = r - nd * kPio2L_2;

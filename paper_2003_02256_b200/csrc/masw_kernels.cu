@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     double *vel = reinterpret_cast<double *>(smem + moff + (unsigned)(N + 1) * sizeof(LayerConst));
 
     Workspace *ws = a.ws;
+    exp_scale_fill();
     if (threadIdx.x == 0) {
         const bool bad = ws_invalid(ws, a.grid_mask, true);
         s_abort = bad;
@@ -586,6 +587,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (ws_invalid(ws, 0x1Fu, true)) return;
+    exp_scale_fill();
     const int N = mod.N;
     LayerConst *lc = reinterpret_cast<LayerConst *>(smem);
     double *vel = reinterpret_cast<double *>(smem + (size_t)(N + 1) * sizeof(LayerConst));
