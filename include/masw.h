@@ -101,6 +101,15 @@ typedef struct {
 #define MASW_SCHED_MODULAR 0x8u
 /* record each team's algorithmic det count (masw_last_team_dets; synchronous calls only) */
 #define MASW_TEAM_STATS 0x10u
+/* Kernel choice for the queue schedule (default: automatic).  Ensembles with many models use
+ * the MODEL-MAJOR scan: a warp takes one model and up to 64 of its wavelengths and computes
+ * the wavelength-free terms of each velocity (wave square roots, half-space element / k)
+ * once for all of them; otherwise the ROW scan (teams of
+ * team_warps warps per (model, lambda) row).  Results are identical.  MASW_SCHED_ROWS forces
+ * the row scan; MASW_SCHED_MODELS forces the model-major scan where its per-warp cache fits
+ * (N <= ~8; else the row scan runs).  With MASW_TEAM_STATS a model-major "team" is a warp. */
+#define MASW_SCHED_ROWS 0x20u
+#define MASW_SCHED_MODELS 0x40u
 
 /* Execution options; a NULL masw_exec means {device = current, stream = legacy default,
  * team_warps = 0 (auto), flags = 0}. */

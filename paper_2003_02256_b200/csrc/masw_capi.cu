@@ -267,10 +267,15 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         const int team = ex.team ? ex.team : auto_team_warps(R, V, dev);
         const int sched = (ex.flags & MASW_SCHED_CONTIGUOUS) ? 1 : ((ex.flags & MASW_SCHED_MODULAR) ? 2 : 0);
         ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws, dce ? 0x7Fu : 0x1Fu, sched, nullptr};
+        // model-major scan for ensembles (auto unless a team size, a static schedule or
+        // MASW_SCHED_ROWS is requested; MASW_SCHED_MODELS forces it where it fits)
+        const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 &&
+                            (((ex.flags & MASW_SCHED_MODELS) && models_scan_suitable(sa, dev, true)) ||
+                             (ex.team == 0 && models_scan_suitable(sa, dev, false)));
         const bool stats = (ex.flags & MASW_TEAM_STATS) != 0 && !(ex.flags & MASW_ASYNC);
         long long nteams = 0;
         if (stats) {
-            nteams = scan_teams(sa, team, dev);
+            nteams = models ? scan_models_warps(sa, dev) : scan_teams(sa, team, dev);
             if (nteams <= 0) return MASW_E_CUDA;
             sa.team_dets = arena.alloc<unsigned long long>((size_t)nteams);
             CK(cudaMemsetAsync(sa.team_dets, 0, nteams * sizeof(unsigned long long), st));
@@ -282,7 +287,11 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
             if (!slot[1]) CK(cudaEventCreate(&slot[1]));
             CK(cudaEventRecord(slot[0], st));
         }
-        CK(launch_scan(sa, team, st, dev));
+        if (models) {
+            CK(launch_scan_models(sa, st, dev));
+        } else {
+            CK(launch_scan(sa, team, st, dev));
+        }
         if (timed) {
             CK(cudaEventRecord(slot[1], st));
             ++t_scan_count;

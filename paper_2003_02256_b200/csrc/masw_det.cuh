@@ -106,16 +106,16 @@ static __constant__ double c_k[6] = {
 
 // 2^(n-1), 2^(-n-1) and their sum and difference (rounded as fp64 addition rounds them) for
 // the cosh/sinh reconstruction, n = 0..511 (th = n ln2 + r <= 350 gives n <= 505): a
-// per-CTA shared-memory table (16 KB) read with two 128-bit loads -- lanes of a warp hold
-// neighbouring velocities, so their n mostly coincide (broadcast).  Filled by
-// exp_scale_fill() at kernel start.
+// per-CTA table at the start of the kernel's dynamic shared memory (16 KB), read with two
+// 128-bit loads -- lanes of a warp hold neighbouring velocities, so their n mostly coincide
+// (broadcast).  Filled by exp_scale_fill() at kernel start.
 struct __align__(16) ExpScale {
     double a, b, apb, amb;
 };
 constexpr int kExpTab = 512;
-static __shared__ ExpScale s_exp_tab[kExpTab];
+constexpr unsigned kExpTabBytes = kExpTab * sizeof(ExpScale);
 
-__device__ __forceinline__ void exp_scale_fill()
+__device__ __forceinline__ void exp_scale_fill(ExpScale *tab)
 {
     for (int n = threadIdx.x; n < kExpTab; n += blockDim.x) {
         const double a = __hiloint2double((n + 1022) << 20, 0);
@@ -125,7 +125,7 @@ __device__ __forceinline__ void exp_scale_fill()
         e.b = b;
         e.apb = a + b;
         e.amb = a - b;
-        s_exp_tab[n] = e;
+        tab[n] = e;
     }
 }
 
@@ -175,7 +175,8 @@ __device__ __forceinline__ double scale2(double x, int k)
 // reciprocal.  With a = 2^(n-1), b = 2^(-n-1):
 //   cosh = (a + b) + a (E + O) + b (E - O)
 //   sinh = (a - b) + a (E + O) - b (E - O)   (= O exactly structured at n = 0: no cancellation)
-__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
+__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh,
+                                          const ExpScale *__restrict__ tab)
 {
     const double t = fma(th, c_k[0], kShifter);
     const double nd = t - kShifter;
@@ -191,7 +192,7 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh)
         po = fma(po, r2, c_expO[i]);
     }
     const double E = pe * r2, O = po * r;
-    const ExpScale S = s_exp_tab[n & (kExpTab - 1)];
+    const ExpScale S = tab[n & (kExpTab - 1)];
     const double ep = E + O, em = E - O;                       // e^r - 1, e^-r - 1
     ch = fma(S.a, ep, fma(S.b, em, S.apb));
     sh = fma(S.a, ep, fma(-S.b, em, S.amb));
@@ -265,12 +266,13 @@ __device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, dou
 
 // -------------------------------------------------------------- wave triples
 // (C, XS, SX) of one wave: q = 1 - c^2/v^2 (!= 0 by S4) and kh = k*h; see header comment.
-__device__ __forceinline__ void wave_hyp(double q, double kh, double &C, double &XS, double &SX)
+__device__ __forceinline__ void wave_hyp(double q, double kh, double &C, double &XS, double &SX,
+                                         const ExpScale *__restrict__ tab)
 {
     double x, rq;                      // x, 1/x
     sqrt_rsqrt(q, x, rq);
     double ch, sh;
-    cosh_sinh(kh * x, ch, sh);
+    cosh_sinh(kh * x, ch, sh, tab);
     C = ch;
     XS = x * sh;
     SX = sh * rq;
@@ -293,10 +295,10 @@ __device__ __forceinline__ void wave_trig(double q, double kh, double &C, double
 }
 
 __device__ __forceinline__ void wave_triple(double q, double kh, double &C, double &XS,
-                                            double &SX)
+                                            double &SX, const ExpScale *__restrict__ tab)
 {
     if (q > 0.0) {
-        wave_hyp(q, kh, C, XS, SX);
+        wave_hyp(q, kh, C, XS, SX, tab);
     } else {
         wave_trig(q, kh, C, XS, SX);
     }
@@ -350,13 +352,15 @@ __device__ __forceinline__ Elem elem_from_triples(double Cr, double XSr, double 
 
 // Rare case c > alpha_e (both waves possibly trigonometric): kept out of line so the hot
 // loop's code stays small (instruction-cache pressure was measured: no_instruction stalls).
-static __device__ __noinline__ void waves_general(double qa, double qb, double kh, double *t)
+static __device__ __noinline__ void waves_general(double qa, double qb, double kh, double *t,
+                                                  const ExpScale *tab)
 {
-    wave_triple(qa, kh, t[0], t[1], t[2]);
-    wave_triple(qb, kh, t[3], t[4], t[5]);
+    wave_triple(qa, kh, t[0], t[1], t[2], tab);
+    wave_triple(qb, kh, t[3], t[4], t[5], tab);
 }
 
-__device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
+__device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
+                                           const ExpScale *__restrict__ tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
     const double qb = fma(-c2, L.ib2, 1.0);   // s^2
@@ -365,19 +369,149 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2)
     // own branch-free copy of the P wave so the two independent chains interleave (ILP).
     if (qa > 0.0) {
         if (qb > 0.0) {
-            wave_hyp(qa, L.kh, Cr, XSr, SXr);
-            wave_hyp(qb, L.kh, Cs, XSs, SXs);
+            wave_hyp(qa, L.kh, Cr, XSr, SXr, tab);
+            wave_hyp(qb, L.kh, Cs, XSs, SXs, tab);
         } else {
-            wave_hyp(qa, L.kh, Cr, XSr, SXr);
+            wave_hyp(qa, L.kh, Cr, XSr, SXr, tab);
             wave_trig(qb, L.kh, Cs, XSs, SXs);
         }
     } else {
         double t[6];
-        waves_general(qa, qb, L.kh, t);
+        waves_general(qa, qb, L.kh, t, tab);
         Cr = t[0]; XSr = t[1]; SXr = t[2];
         Cs = t[3]; XSs = t[4]; SXs = t[5];
     }
     return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2);
+}
+
+// -------------------------------------------------------------- wavelength-free terms
+// The square roots r_e = sqrt(1 - c^2/alpha_e^2), s_e = sqrt(1 - c^2/beta_e^2) and the
+// half-space's k-free factors depend on the model and c but NOT on the wavelength, so the
+// model-major scan (scan_models_kernel) computes them once per (model, c) for all of a
+// model's wavelengths.  Everything downstream is evaluated with the same operations in the
+// same order as in the row scan, so both give bitwise-identical determinants.  A root is
+// stored as (x, 1/|x|) with x = +sqrt(q) for a hyperbolic wave (q > 0) and x = -sqrt(-q)
+// for a trigonometric one.
+__device__ __forceinline__ double2 wave_root(double q)
+{
+    double x, rx;
+    sqrt_rsqrt(fabs(q), x, rx);
+    return make_double2(q > 0.0 ? x : -x, rx);
+}
+
+__device__ __forceinline__ void wave_hyp_root(double x, double rx, double kh, double &C,
+                                              double &XS, double &SX,
+                                              const ExpScale *__restrict__ tab)
+{
+    double ch, sh;
+    cosh_sinh(kh * x, ch, sh, tab);
+    C = ch;
+    XS = x * sh;
+    SX = sh * rx;
+}
+
+__device__ __forceinline__ void wave_trig_root(double xneg, double rx, double kh, double &C,
+                                               double &XS, double &SX)
+{
+    const double xi = -xneg;
+    const double th = kh * xi;
+    double sn, cs;
+    if (th < kTrigMax) {
+        sin_cos(th, sn, cs);
+    } else {
+        sin_cos_large(th, sn, cs);
+    }
+    C = cs;
+    XS = -xi * sn;
+    SX = sn * rx;
+}
+
+// Element of layer M at wavenumber k from the cached roots a (P wave) and b (S wave).  M holds
+// the model's k-free constants: M.kh = h, M.krho = rho, M.mu = beta^2 (k h, k rho and
+// mu = (k rho) beta^2 are formed here exactly as the row scan's LayerConst fill forms them).
+__device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, double2 a,
+                                                double2 b, double c2,
+                                                const ExpScale *__restrict__ tab)
+{
+    const double kh = k * M.kh;
+    const double krho = k * M.krho;
+    double Cr, XSr, SXr, Cs, XSs, SXs;
+    if (a.x > 0.0) {
+        if (b.x > 0.0) {
+            wave_hyp_root(a.x, a.y, kh, Cr, XSr, SXr, tab);
+            wave_hyp_root(b.x, b.y, kh, Cs, XSs, SXs, tab);
+        } else {
+            wave_hyp_root(a.x, a.y, kh, Cr, XSr, SXr, tab);
+            wave_trig_root(b.x, b.y, kh, Cs, XSs, SXs);
+        }
+    } else {
+        double t[6];
+        waves_general(fma(-c2, M.ia2, 1.0), fma(-c2, M.ib2, 1.0), kh, t, tab);
+        Cr = t[0]; XSr = t[1]; SXr = t[2];
+        Cs = t[3]; XSs = t[4]; SXs = t[5];
+    }
+    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, krho, krho * M.mu, c2);
+}
+
+// Half-space element K_hs = mu [[r w/(1-rs), w/(1-rs) - 2], [., s w/(1-rs)]], w = 1 - s^2 =
+// c^2/beta_N^2 (real), mu = k rho_N beta_N^2; cases by the branch of r, s (reading S3).
+// Split into the k-free factors (HsRoot: the roots, gw = w/(1 - r s) or its analogue, and
+// the case) and the mu-dependent entries.
+struct HalfSpace {
+    double h11r, h11i, h12r, h12i, h22r, h22i;
+};
+struct HsRoot {
+    double r, s, gw, t;
+    int kase;   // 0: c < beta_N (r, s real); 1: beta_N < c < alpha_N (s = i xs); 2: c > alpha_N
+};
+
+__device__ __forceinline__ HsRoot halfspace_root(double ia2, double ib2, double c2)
+{
+    HsRoot R;
+    const double qa = fma(-c2, ia2, 1.0), qb = fma(-c2, ib2, 1.0);
+    const double w = c2 * ib2;
+    if (qb > 0.0) {
+        R.r = qa * rsqrt_fast(qa);
+        R.s = qb * rsqrt_fast(qb);
+        R.gw = w * rcp_fast(1.0 - R.r * R.s);
+        R.t = 0.0;
+        R.kase = 0;
+    } else if (qa > 0.0) {
+        R.r = qa * rsqrt_fast(qa);
+        R.s = -qb * rsqrt_fast(-qb);          // xs
+        R.t = R.r * R.s;                       // 1/(1 - i t) = (1 + i t)/(1 + t^2)
+        R.gw = w * rcp_fast(fma(R.t, R.t, 1.0));
+        R.kase = 1;
+    } else {
+        R.r = -qa * rsqrt_fast(-qa);          // xr
+        R.s = -qb * rsqrt_fast(-qb);          // xs
+        R.gw = w * rcp_fast(fma(R.r, R.s, 1.0));
+        R.t = 0.0;
+        R.kase = 2;
+    }
+    return R;
+}
+
+__device__ __forceinline__ HalfSpace halfspace_k(const HsRoot &R, double mu)
+{
+    HalfSpace H;
+    if (R.kase == 0) {
+        const double g = mu * R.gw;
+        H.h11r = R.r * g; H.h11i = 0.0;
+        H.h12r = g - 2.0 * mu; H.h12i = 0.0;
+        H.h22r = R.s * g; H.h22i = 0.0;
+    } else if (R.kase == 1) {
+        const double gre = mu * R.gw, gim = gre * R.t;
+        H.h11r = R.r * gre; H.h11i = R.r * gim;
+        H.h12r = gre - 2.0 * mu; H.h12i = gim;
+        H.h22r = -R.s * gim; H.h22i = R.s * gre;
+    } else {
+        const double g = mu * R.gw;
+        H.h11r = 0.0; H.h11i = R.r * g;
+        H.h12r = g - 2.0 * mu; H.h12i = 0.0;
+        H.h22r = 0.0; H.h22i = R.s * g;
+    }
+    return H;
 }
 
 // -------------------------------------------------------------- determinant
@@ -534,8 +668,8 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
     return o;
 }
 
-// Determinant of K(k, c) for one row whose LayerConst[0..N] and velocity list are in `lc`,
-// `vel` (shared memory).  c is the unperturbed grid value.
+// Determinant core (sign, optionally value) of K for N layers.  elem(e) returns the element
+// of layer e (0 <= e < N), hs() the half-space element.
 //
 // Elimination (reading S10/S11): banded GEPP streamed node by node.  The nodes' rows hold
 //   node 0:     [ top_0 | B_0 ]
@@ -547,18 +681,12 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
 // (reading S3/S5), so the pivots and all but the last node's columns are real fp64; only
 // node N's columns (K_hs) are complex.  det K = (-1)^parity * prod pivots * det(last 2x2).
 // Cost per node: one layer element + one 4-row GEPP step, O(N) in total.
-// `maybe_near` = false means c is already the S4-perturbed velocity (the scan resolves S4
-// per warp for its 32 velocities, see scan_kernel), which skips the per-lane S4 loop.
-// NFIX > 0 compiles the determinant for exactly NFIX layers (fully unrolled: no loop-carried
-// register copies, constant shared-memory offsets); NFIX = 0 takes N at run time.
-template <bool WANT_VALUE, int NFIX = 0>
-__device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
-                                        const double *__restrict__ vel, int Nrt, double c,
-                                        bool maybe_near = true)
+// NFIX > 0 compiles the determinant for exactly NFIX layers (fully unrolled); NFIX = 0 takes
+// N at run time.
+template <bool WANT_VALUE, int NFIX, class ElemFn, class HsFn>
+__device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
 {
     const int N = NFIX > 0 ? NFIX : Nrt;
-    const double cp = maybe_near ? perturb_velocity(vel, 2 * (N + 1), c) : c;
-    const double c2 = cp * cp;
 
     // Sign, zero and non-finite bookkeeping in integer ops on the pivots' high words (off the
     // FP64 pipe): sgn accumulates the XOR of the pivots' sign bits; a zero pivot has key 0, an
@@ -569,11 +697,11 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     int kmin = 0x7fffffff, kmax = 0;
     DetAcc acc{1.0, 0};
 
-    Elem P = layer_elem(load_lc(lc), c2);
+    Elem P = elem(0);
     double X[2][4] = {{P.k11, P.k12, P.k13, P.k14}, {P.k12, P.k22, -P.k14, P.k24}};
 
     auto node_step = [&](int t) {
-        const Elem Q = layer_elem(load_lc(lc + t + 1), c2);
+        const Elem Q = elem(t + 1);
         double R[4][6] = {
             {X[0][0], X[0][1], X[0][2], X[0][3], 0.0, 0.0},
             {X[1][0], X[1][1], X[1][2], X[1][3], 0.0, 0.0},
@@ -601,45 +729,17 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
         for (int t = 0; t + 1 < N; ++t) node_step(t);
     }
 
-    // Half-space K_hs = mu [[r w/(1-rs), w/(1-rs) - 2], [., s w/(1-rs)]], w = 1 - s^2 =
-    // c^2/beta_N^2 (real); cases by the branch of r, s (reading S3).
-    double h11r, h11i, h12r, h12i, h22r, h22i;
-    {
-        const LayerConst H = load_lc(lc + N);
-        const double ia2 = H.ia2, ib2 = H.ib2, mu = H.mu;
-        const double qa = fma(-c2, ia2, 1.0), qb = fma(-c2, ib2, 1.0);
-        const double w = c2 * ib2;
-        if (qb > 0.0) {                     // c < beta_N < alpha_N: r, s real
-            const double r = qa * rsqrt_fast(qa), s = qb * rsqrt_fast(qb);
-            const double g = mu * (w * rcp_fast(1.0 - r * s));
-            h11r = r * g; h11i = 0.0;
-            h12r = g - 2.0 * mu; h12i = 0.0;
-            h22r = s * g; h22i = 0.0;
-        } else if (qa > 0.0) {              // beta_N < c < alpha_N: r real, s = i xs
-            const double r = qa * rsqrt_fast(qa), xs = -qb * rsqrt_fast(-qb);
-            const double t = r * xs;        // 1/(1 - i t) = (1 + i t)/(1 + t^2)
-            const double gre = mu * (w * rcp_fast(fma(t, t, 1.0))), gim = gre * t;
-            h11r = r * gre; h11i = r * gim;
-            h12r = gre - 2.0 * mu; h12i = gim;
-            h22r = -xs * gim; h22i = xs * gre;
-        } else {                            // c > alpha_N: r = i xr, s = i xs
-            const double xr = -qa * rsqrt_fast(-qa), xs = -qb * rsqrt_fast(-qb);
-            const double g = mu * (w * rcp_fast(fma(xr, xs, 1.0)));
-            h11r = 0.0; h11i = xr * g;
-            h12r = g - 2.0 * mu; h12i = 0.0;
-            h22r = 0.0; h22i = xs * g;
-        }
-    }
+    const HalfSpace H = hs();
 
     // Last step: node N-1 columns real, node N columns complex (NR = 2).
     double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
                       {X[1][0], X[1][1], X[1][2], X[1][3]},
-                      {P.k13, -P.k14, P.k11 + h11r, h12r - P.k12},
-                      {P.k14, P.k24, h12r - P.k12, P.k22 + h22r}};
+                      {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
+                      {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
     double Ri[4][4] = {{0.0, 0.0, 0.0, 0.0},
                        {0.0, 0.0, 0.0, 0.0},
-                       {0.0, 0.0, h11i, h12i},
-                       {0.0, 0.0, h12i, h22i}};
+                       {0.0, 0.0, H.h11i, H.h12i},
+                       {0.0, 0.0, H.h12i, H.h22i}};
     double Y[2][2], Yi[2][2];
     const StepOut so = gepp_step<4, 2>(R, Ri, Y, Yi);
     sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
@@ -684,6 +784,27 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
         }
     }
     return out;
+}
+
+// det K(k, c) for one row whose LayerConst[0..N] (k-scaled) and velocity list are in `lc`,
+// `vel` (shared memory).  `maybe_near` = false means c is already the S4-perturbed velocity
+// (the scan resolves S4 per warp for its 32 velocities, see scan_kernel), which skips the
+// per-lane S4 loop.
+template <bool WANT_VALUE, int NFIX = 0>
+__device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
+                                        const double *__restrict__ vel,
+                                        const ExpScale *__restrict__ tab, int Nrt, double c,
+                                        bool maybe_near = true)
+{
+    const int N = NFIX > 0 ? NFIX : Nrt;
+    const double cp = maybe_near ? perturb_velocity(vel, 2 * (N + 1), c) : c;
+    const double c2 = cp * cp;
+    return det_core<WANT_VALUE, NFIX>(
+        N, [&](int e) { return layer_elem(load_lc(lc + e), c2, tab); },
+        [&] {
+            const LayerConst H = load_lc(lc + N);
+            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.mu);
+        });
 }
 
 

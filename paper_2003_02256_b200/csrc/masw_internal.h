@@ -64,6 +64,12 @@ cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, co
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
                             cudaStream_t st);
 int auto_team_warps(int64_t rows, int64_t V, int device);
+// Model-major scan (ensembles): suitable when there are many (model, wavelength-block) items
+// and the per-warp caches fit two CTAs per SM; same outputs as launch_scan.
+bool models_scan_suitable(const ScanArgs &a, int device, bool forced);
+cudaError_t launch_scan_models(const ScanArgs &a, cudaStream_t st, int device,
+                               long long *warps_out = nullptr);
+long long scan_models_warps(const ScanArgs &a, int device);
 
 void count_launch();
 long long launches();

@@ -203,14 +203,16 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int team = warp / TEAM, wt = warp % TEAM, tl = wt * 32 + lane;
 
-    TeamCtrl *ctrl = reinterpret_cast<TeamCtrl *>(smem) + team;
-    const unsigned moff = round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
+    // dynamic shared memory: [cosh/sinh scale table | team controls | per-team row constants]
+    ExpScale *tab = reinterpret_cast<ExpScale *>(smem);
+    TeamCtrl *ctrl = reinterpret_cast<TeamCtrl *>(smem + kExpTabBytes) + team;
+    const unsigned moff = kExpTabBytes + round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
                           (unsigned)team * team_model_bytes(N);
     LayerConst *lc = reinterpret_cast<LayerConst *>(smem + moff);
     double *vel = reinterpret_cast<double *>(smem + moff + (unsigned)(N + 1) * sizeof(LayerConst));
 
     Workspace *ws = a.ws;
-    exp_scale_fill();
+    exp_scale_fill(tab);
     if (threadIdx.x == 0) {
         const bool bad = ws_invalid(ws, a.grid_mask, true);
         s_abort = bad;
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             x.ia2 = 1.0 / (al * al);
             x.ib2 = 1.0 / (be * be);
             x.krho = k * rh;
-            x.mu = k * rh * be * be;
+            x.mu = x.krho * (be * be);   // (k rho) beta^2, as layer_elem_root forms it
             x.pad = 0.0;
             lc[e] = x;
             vel[2 * e] = al;
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             int s = 0;
             bool bad = false;
             if (j < V) {
-                const DetOut d = det_K<false, NFIX>(lc, vel, N, c, false);
+                const DetOut d = det_K<false, NFIX>(lc, vel, tab, N, c, false);
                 s = d.sign;
                 bad = d.bad;
                 ++my_eval;
@@ -378,6 +380,203 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     }
 }
 
+// ------------------------------------------------------------------ model-major scan
+// For ensembles (many models): a warp takes a WORK ITEM = one model and up to kModelRows of
+// its wavelengths, and scans the velocity chunks in ascending order for all of the item's
+// rows that have not found their first sign change yet.  Per chunk each lane computes the
+// wavelength-free terms of its velocity once (the P/S square roots of every layer and the
+// half-space element / k, see wave_root and halfspace in masw_det.cuh) into warp-private
+// shared memory, and reuses them for every active row -- each row's determinant then needs
+// only its k h_e-dependent part.  Results are those of scan_kernel (same algorithm per row,
+// K^ = K / k has the sign of K).
+constexpr int kModelRows = 64;
+
+__host__ __device__ inline unsigned warp_model_bytes(int N)
+{
+    return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
+                   2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
+                   (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
+                   2u * (unsigned)N * 32u * 16u +                          // roots P, S [e][lane]
+                   2u * 32u * 16u + 32u * 4u);                             // half-space, case
+}
+
+__global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_abort;
+
+    const int N = a.mod.N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    ExpScale *tab = reinterpret_cast<ExpScale *>(smem);
+    unsigned char *wb = smem + kExpTabBytes + (unsigned)warp * warp_model_bytes(N);
+    LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
+    double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
+    double *kr = vel + 2 * (N + 1);
+    double2 *RA = reinterpret_cast<double2 *>(kr + kModelRows);   // P-wave roots [e][lane]
+    double2 *RB = RA + 32 * N;                                     // S-wave roots [e][lane]
+    double2 *HS = RB + 32 * N;                                     // half-space [2][lane]
+    int *HK = reinterpret_cast<int *>(HS + 64);                    // half-space case [lane]
+
+    Workspace *ws = a.ws;
+    exp_scale_fill(tab);
+    if (threadIdx.x == 0) {
+        const bool bad = ws_invalid(ws, a.grid_mask, true);
+        s_abort = bad;
+        if (bad && blockIdx.x == 0) ws->abort = 1;
+    }
+    __syncthreads();
+    if (s_abort) return;
+
+    const int64_t M = a.mod.M, L = a.L, V = a.V;
+    const int64_t groups = (L + kModelRows - 1) / kModelRows;
+    const int64_t items = M * groups;
+    const double *__restrict__ cg = a.c;
+    const int nv = 2 * (N + 1);
+    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0;
+    unsigned my_status = 0;
+
+    for (;;) {
+        long long item;
+        if (lane == 0) item = (long long)atomicAdd(&ws->queue, 1ull);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= items) break;
+        const int64_t m = item / groups;
+        const int64_t i0 = (item - m * groups) * kModelRows;
+        const int nr = (int)min((int64_t)kModelRows, L - i0);
+
+        // model constants without the wavenumber: h, 1/alpha^2, 1/beta^2, rho, beta^2
+        for (int e = lane; e <= N; e += 32) {
+            const double al = a.mod.alpha[m * (N + 1) + e];
+            const double be = a.mod.beta[m * (N + 1) + e];
+            const double rh = a.mod.rho[m * (N + 1) + e];
+            LayerConst x;
+            x.kh = (e < N) ? a.mod.h[m * N + e] : 0.0;
+            x.ia2 = 1.0 / (al * al);
+            x.ib2 = 1.0 / (be * be);
+            x.krho = rh;
+            x.mu = be * be;
+            x.pad = 0.0;
+            mc[e] = x;
+            vel[2 * e] = al;
+            vel[2 * e + 1] = be;
+        }
+        for (int r = lane; r < nr; r += 32) kr[r] = kTwoPi / a.lam[i0 + r];   // reading S2
+        __syncwarp();
+
+        const unsigned long long all = (nr == 64) ? ~0ull : ((1ull << nr) - 1ull);
+        unsigned long long done = 0, cpos = 0, cneg = 0;   // per row: found, carry sign
+        for (int64_t base = 0; base < V && done != all; base += 32) {
+            const int64_t j = base + lane;
+            const bool valid = j < V;
+            double c = cg[valid ? j : V - 1];
+            {   // reading S4, as in scan_kernel
+                const double clo = __shfl_sync(FULL, c, 0) - 1e-3;
+                const double chi = __shfl_sync(FULL, c, 31) + 1e-3;
+                bool lane_near = false;
+                for (int e0 = 0; e0 < nv; e0 += 32) {
+                    bool in = false;
+                    if (e0 + lane < nv) {
+                        const double v = vel[e0 + lane];
+                        in = (v > clo) && (v < chi);
+                    }
+                    for (unsigned b = __ballot_sync(FULL, in); b; b &= b - 1)
+                        lane_near |= fabs(c - vel[e0 + __ffs(b) - 1]) < kPerturbTol;
+                }
+                if (lane_near) c = perturb_velocity(vel, nv, c);
+            }
+            const double c2 = c * c;
+            // wavelength-free terms of this lane's velocity (lane-private slots: no sync)
+            for (int e = 0; e < N; ++e) {
+                const LayerConst Lc = load_lc(mc + e);
+                RA[e * 32 + lane] = wave_root(fma(-c2, Lc.ia2, 1.0));
+                RB[e * 32 + lane] = wave_root(fma(-c2, Lc.ib2, 1.0));
+            }
+            {
+                const LayerConst Hl = load_lc(mc + N);
+                const HsRoot h = halfspace_root(Hl.ia2, Hl.ib2, c2);
+                HS[lane] = make_double2(h.r, h.s);
+                HS[32 + lane] = make_double2(h.gw, h.t);
+                HK[lane] = h.kase;
+            }
+            const LayerConst Hl = load_lc(mc + N);
+            for (unsigned long long pend = all & ~done; pend; pend &= pend - 1) {
+                const int r = __ffsll((long long)pend) - 1;
+                const double k = kr[r];
+                int s = 0;
+                bool bad = false;
+                if (valid) {
+                    const DetOut d = det_core<false, 0>(
+                        N,
+                        [&](int e) {
+                            return layer_elem_root(load_lc(mc + e), k, RA[e * 32 + lane],
+                                                   RB[e * 32 + lane], c2, tab);
+                        },
+                        [&] {
+                            const double2 rs = HS[lane], gt = HS[32 + lane];
+                            HsRoot h;
+                            h.r = rs.x;
+                            h.s = rs.y;
+                            h.gw = gt.x;
+                            h.t = gt.y;
+                            h.kase = HK[lane];
+                            return halfspace_k(h, (k * Hl.krho) * Hl.mu);
+                        });
+                    s = d.sign;
+                    bad = d.bad;
+                    ++my_eval;
+                }
+                int sprev = __shfl_up_sync(FULL, s, 1);
+                if (lane == 0) sprev = ((cpos >> r) & 1ull) ? 1 : (((cneg >> r) & 1ull) ? -1 : 0);
+                const bool ev = valid && (bad || (j > 0 && s != sprev));
+                const unsigned mask = __ballot_sync(FULL, ev);
+                if (mask) {
+                    const int64_t first = base + (__ffs(mask) - 1);
+                    if (j == first) {
+                        const int64_t o = m * L + i0 + r;
+                        if (bad) {
+                            a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+                            if (a.idx) a.idx[o] = -2;
+                            my_status |= 2u;
+                        } else {
+                            a.ct[o] = cg[j];
+                            if (a.idx) a.idx[o] = (int32_t)j;
+                        }
+                        my_alg += (unsigned long long)(j + 1);
+                    }
+                    team_alg += (unsigned long long)(first + 1);
+                    done |= 1ull << r;
+                } else {
+                    const int last = __shfl_sync(FULL, s, 31);
+                    cpos = (cpos & ~(1ull << r)) | ((unsigned long long)(last > 0) << r);
+                    cneg = (cneg & ~(1ull << r)) | ((unsigned long long)(last < 0) << r);
+                }
+            }
+        }
+        for (unsigned long long pend = all & ~done; pend; pend &= pend - 1) {
+            const int r = __ffsll((long long)pend) - 1;
+            team_alg += (unsigned long long)V;
+            if (lane == 0) {
+                const int64_t o = m * L + i0 + r;
+                a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+                if (a.idx) a.idx[o] = -1;
+                my_status |= 1u;
+                my_alg += (unsigned long long)V;
+            }
+        }
+        __syncwarp();   // the next item rewrites this warp's constants
+    }
+    if (a.team_dets && lane == 0) a.team_dets[(long long)blockIdx.x * 8 + warp] = team_alg;
+
+    my_alg = warp_sum_u64(my_alg);
+    my_eval = warp_sum_u64(my_eval);
+    my_status = __reduce_or_sync(FULL, my_status);
+    if (lane == 0) {
+        if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
+        if (my_eval) atomicAdd(&ws->eval_dets, my_eval);
+        if (my_status) atomicOr(&ws->row_status, my_status);
+    }
+}
+
 // Per-device launch facts, cached: SM count and resident CTAs per SM per (kernel, smem).
 namespace {
 std::mutex g_cache_mu;
@@ -414,7 +613,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
                                  long long *teams_out, bool dry = false)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
-    const size_t smem = round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
+    const size_t smem = kExpTabBytes + round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
                         (size_t)TEAMS * team_model_bytes(a.mod.N);
     auto kern = scan_kernel<TEAM, BLOCK, NFIX>;
     const int sms = sm_count(device);
@@ -479,6 +678,89 @@ long long scan_teams(const ScanArgs &a, int team_warps, int device)
     long long t = 0;
     if (dispatch_scan(a, team_warps, nullptr, device, &t, true) != cudaSuccess) return -1;
     return t;
+}
+
+// Model-major launch: one work item per (model, block of kModelRows wavelengths).
+static size_t models_smem(int N) { return kExpTabBytes + 8u * (size_t)warp_model_bytes(N); }
+
+static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
+                                 long long *warps_out, bool dry, int *per_sm_out = nullptr)
+{
+    const size_t smem = models_smem(a.mod.N);
+    auto kern = scan_models_kernel;
+    const int sms = sm_count(device);
+    const long long key = ((long long)device << 48) | (1ll << 47) | (long long)smem;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        auto it = g_occ_cache.find(key);
+        if (it != g_occ_cache.end()) per_sm = it->second;
+    }
+    if (per_sm == 0) {
+        // a cache that does not fit is "0 CTAs per SM", not an error (and must not leave a
+        // pending runtime error for the next launch's cudaGetLastError)
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        const size_t static_smem = 16;
+        if (smem + static_smem > (size_t)optin) {
+            per_sm = -1;
+        } else {
+            if (smem > 48 * 1024 &&
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem) != cudaSuccess) {
+                cudaGetLastError();
+                per_sm = -1;
+            } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) !=
+                       cudaSuccess) {
+                cudaGetLastError();
+                per_sm = -1;
+            }
+            if (per_sm == 0) per_sm = -1;
+        }
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        g_occ_cache[key] = per_sm;
+    }
+    if (per_sm < 0) per_sm = 0;
+    if (per_sm_out) *per_sm_out = per_sm;
+    if (per_sm == 0) return cudaErrorInvalidConfiguration;
+    const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = (items + 7) / 8;
+    if (need < blocks) blocks = need;
+    if (blocks < 1) blocks = 1;
+    if (warps_out) *warps_out = blocks * 8;
+    if (dry) return cudaSuccess;
+    kern<<<(unsigned)blocks, 256, smem, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
+{
+    // unless forced: enough work items to fill the GPU several times over, several
+    // wavelengths per model to share the cache, and two 256-thread CTAs per SM with the
+    // per-warp caches (N <= ~8)
+    const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
+    const int sms = sm_count(device);
+    if (a.sched != 0) return false;
+    if (!forced && (items < 4ll * sms * 16 || a.L < 8)) return false;
+    int per_sm = 0;
+    long long w = 0;
+    if (launch_models(a, nullptr, device, &w, true, &per_sm) != cudaSuccess) return false;
+    return per_sm >= (forced ? 1 : 2);
+}
+
+cudaError_t launch_scan_models(const ScanArgs &a, cudaStream_t st, int device,
+                               long long *warps_out)
+{
+    return launch_models(a, st, device, warps_out, false);
+}
+
+long long scan_models_warps(const ScanArgs &a, int device)
+{
+    long long w = 0;
+    if (launch_models(a, nullptr, device, &w, true) != cudaSuccess) return -1;
+    return w;
 }
 
 // ------------------------------------------------------------------ misfit (Algorithm 2)
@@ -587,10 +869,11 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (ws_invalid(ws, 0x1Fu, true)) return;
-    exp_scale_fill();
+    ExpScale *tab = reinterpret_cast<ExpScale *>(smem);
+    exp_scale_fill(tab);
     const int N = mod.N;
-    LayerConst *lc = reinterpret_cast<LayerConst *>(smem);
-    double *vel = reinterpret_cast<double *>(smem + (size_t)(N + 1) * sizeof(LayerConst));
+    LayerConst *lc = reinterpret_cast<LayerConst *>(smem + kExpTabBytes);
+    double *vel = reinterpret_cast<double *>(smem + kExpTabBytes + (size_t)(N + 1) * sizeof(LayerConst));
     const int64_t i = blockIdx.y;
     const double k = kTwoPi / lam[i];
     for (int e = threadIdx.x; e <= N; e += blockDim.x) {
@@ -600,7 +883,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
         x.ia2 = 1.0 / (al * al);
         x.ib2 = 1.0 / (be * be);
         x.krho = k * rh;
-        x.mu = k * rh * be * be;
+        x.mu = x.krho * (be * be);   // (k rho) beta^2, as layer_elem_root forms it
         x.pad = 0.0;
         lc[e] = x;
         vel[2 * e] = al;
@@ -609,7 +892,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
     __syncthreads();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
-    const DetOut d = det_K<true>(lc, vel, N, c[j]);
+    const DetOut d = det_K<true>(lc, vel, tab, N, c[j]);
     const int64_t o = i * V + j;
     mre[o] = d.mre;
     mim[o] = d.mim;
@@ -620,7 +903,7 @@ cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, co
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
                             cudaStream_t st)
 {
-    const size_t smem = team_model_bytes(m.N);
+    const size_t smem = kExpTabBytes + team_model_bytes(m.N);
     dim3 grid((unsigned)((V + 255) / 256), (unsigned)L);
     det_grid_kernel<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws);
     count_launch();

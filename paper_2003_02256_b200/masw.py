@@ -23,6 +23,7 @@ E_ARG, E_MODEL, E_GRID, E_RANGE, E_NONFINITE, E_CUDA, E_NOMEM = -1, -2, -3, -4, 
 IDX_NO_CHANGE, IDX_NONFINITE = -1, -2
 ASYNC, TIME_SCAN = 0x1, 0x2
 SCHED_CONTIGUOUS, SCHED_MODULAR, TEAM_STATS = 0x4, 0x8, 0x10
+SCHED_ROWS, SCHED_MODELS = 0x20, 0x40   # force the row / model-major scan kernel
 MAX_LAYERS = 64
 
 

@@ -35,6 +35,7 @@ def main():
         tf, ms = masw.masw_probe_fp64_peak(-1, 300.0)
         print(f"fp64 probe: {tf:.2f} TFLOP/s ({ms:.1f} ms)", flush=True)
     team_env = int(os.environ.get("TEAM", "0"))
+    xflags = int(os.environ.get("FLAGS", "0"), 0)   # e.g. FLAGS=0x20 (rows) / 0x40 (models)
     only = os.environ.get("CONFIGS", "tiny,maswaves,uniform,realistic,ensemble").split(",")
     for name, kw in [("tiny", {}), ("maswaves", {}), ("uniform", {"tier": 200.0}),
                      ("realistic", {}), ("ensemble", {"M": 100_000})]:
@@ -45,10 +46,10 @@ def main():
         args = [dev(x) for x in (m.h, m.alpha, m.beta, m.rho)]
         lam, c = dev(w.lam), dev(w.c)
         ce = dev(w.ce) if w.ce is not None else None
-        for team in ([team_env] if team_env else [0, 1, 2, 4, 8]):
+        for team in ([team_env] if team_env >= 0 else [0]) if "TEAM" in os.environ else [0, 1, 2, 4, 8]:
             if name == "ensemble":
                 fn = lambda: masw.masw_curves_ensemble(*args, lam, c, ce, team_warps=team,
-                                                       flags=masw.TIME_SCAN)
+                                                       flags=masw.TIME_SCAN | xflags)
             else:
                 fn = lambda: masw.masw_curve(*[a[0] for a in args], lam, c, team_warps=team,
                                              flags=masw.TIME_SCAN)

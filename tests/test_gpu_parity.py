@@ -275,6 +275,86 @@ def test_ensemble_edge_cases(masw, orc):
     assert np.array_equal(r.idx, o["idx"]) and r.status == o["status"]
 
 
+# ------------------------------------------------------------------ model-major scan
+
+def _ens(masw, mods, lam, c, ce, flags, device=False):
+    if device:
+        args = [dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)] + [dev(lam), dev(c)]
+        r = masw.masw_curves_ensemble(*args, dev(ce) if ce is not None else None, flags=flags)
+        return (r.status, r.ct.cpu().numpy(), r.idx.cpu().numpy(),
+                r.misfit.cpu().numpy() if r.misfit is not None else None)
+    r = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, lam, c, ce, flags=flags)
+    return r.status, r.ct, r.idx, r.misfit
+
+
+@pytest.mark.parametrize("L", [1, 3, 40, 64, 65, 130])
+def test_models_kernel_bitwise_equals_row_kernel(masw, L):
+    """The model-major scan (per-(model, c) roots shared by up to 64 wavelengths) computes
+    every determinant with the row scan's operations in the row scan's order: identical
+    C_t, idx and misfit, for one and several wavelength blocks per model and ragged tails."""
+    w = synth.workload("ensemble", M=97)
+    mods = w.models
+    lam = synth.geom(40.0, 1.0, L) if L > 1 else np.array([7.5])
+    ce = np.interp(lam, w.lam[::-1], w.ce[::-1])
+    rows = _ens(masw, mods, lam, w.c, ce, masw.SCHED_ROWS)
+    mm = _ens(masw, mods, lam, w.c, ce, masw.SCHED_MODELS, device=True)
+    assert rows[0] == mm[0]
+    assert np.array_equal(rows[2], mm[2])
+    assert np.array_equal(rows[1], mm[1], equal_nan=True)
+    assert np.array_equal(rows[3], mm[3])
+
+
+def test_models_kernel_oracle_parity(masw, orc):
+    w = synth.workload("ensemble", M=150)
+    mods = w.models
+    st, ct, idx, mis = _ens(masw, mods, w.lam, w.c, w.ce, masw.SCHED_MODELS)
+    o = orc.ensemble(mods, w.lam, w.c, w.ce)
+    assert st == o["status"]
+    for m in range(mods.n_models):
+        ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), w.lam, w.c, idx[m], o["idx"][m])
+        assert ok.all(), m
+        assert parity.misfit_ok(orc, ct[m], w.ce, mis[m])
+
+
+def test_models_kernel_no_change_rows_and_stats(masw, orc):
+    """Rows without a sign change (idx -1, status WARN) on a grid ending below C_t, V not a
+    multiple of 32, per-warp det counts summing to the algorithmic count."""
+    w = synth.workload("ensemble", M=40)
+    mods = w.models
+    c = 20.0 + 0.37 * np.arange(171, dtype=np.float64)       # 20 .. 82.9 m/s
+    r_rows = _ens(masw, mods, w.lam, c, None, masw.SCHED_ROWS)
+    r = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, w.lam, c, None,
+                                  flags=masw.SCHED_MODELS | masw.TEAM_STATS)
+    o = orc.ensemble(mods, w.lam, c)
+    assert r.status == o["status"] == r_rows[0]
+    assert np.array_equal(r.idx, r_rows[2]) and (r.idx == -1).any() and (r.idx >= 0).any()
+    for m in range(mods.n_models):
+        ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), w.lam, c, r.idx[m], o["idx"][m])
+        assert ok.all()
+    alg, ev = masw.masw_last_work()
+    per = masw.masw_last_team_dets()
+    assert per.sum() == alg
+    want = np.where(r.idx >= 0, r.idx + 1, len(c)).sum()
+    assert alg == want
+
+
+def test_models_kernel_deep_stack_falls_back(masw):
+    """N = 24: the per-warp cache does not fit two CTAs per SM; MASW_SCHED_MODELS then runs
+    where it fits (one CTA per SM) or the row scan -- results are the same either way."""
+    N = 24
+    rng = np.random.default_rng(5)
+    M = 6
+    h = rng.uniform(0.5, 2.0, (M, N))
+    beta = rng.uniform(100.0, 400.0, (M, N + 1))
+    alpha = np.full((M, N + 1), 1440.0)
+    rho = np.full((M, N + 1), 1900.0)
+    lam = synth.geom(30.0, 2.0, 12)
+    c = 10.0 + 0.5 * np.arange(900, dtype=np.float64)
+    a = masw.masw_curves_ensemble(h, alpha, beta, rho, lam, c, flags=masw.SCHED_ROWS)
+    b = masw.masw_curves_ensemble(h, alpha, beta, rho, lam, c, flags=masw.SCHED_MODELS)
+    assert np.array_equal(a.idx, b.idx) and a.status == b.status
+
+
 @pytest.mark.slow
 def test_ensemble_full_size_sampled(masw, orc):
     """C5 at full size (100k models) through the device path bench.py times; the oracle
