@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmasw.so")
 SOURCES = ["masw_kernels.cu", "masw_capi.cu", "masw_probe.cu"]
-HEADERS = ["masw_det.cuh", "masw_internal.h"]
+HEADERS = ["masw_det.cuh", "masw_exp_table.h", "masw_internal.h"]
 PUBLIC_HEADERS = [os.path.join(ROOT, "include", "masw.h"), os.path.join(ROOT, "include", "masw_probe.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

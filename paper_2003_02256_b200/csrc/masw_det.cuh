@@ -29,6 +29,8 @@
 
 #include <cstdint>
 
+#include "masw_exp_table.h"
+
 #ifndef MASW_LAYER_UNROLL
 #define MASW_LAYER_UNROLL 1
 #endif
@@ -74,14 +76,8 @@ __device__ __forceinline__ LayerConst load_lc(const LayerConst *p)
 //
 // Near-minimax (Chebyshev-fitted, coefficients rounded to fp64; scripts/minimax_coeffs.py)
 // polynomials in u = r^2, highest degree first.  Max relative error with these fp64
-// coefficients (50-digit check): e^r even part E/u 4e-19 and odd part O/r 1.4e-18 on
-// |r| <= ln2/2; sin(r)/r 1.3e-17 and cos(r) 7.2e-18 on |r| <= pi/4.
-static __constant__ double c_expE[6] = {2.0918129454967065e-09, 2.755726330147475e-07,
-                                        2.480158733642132e-05, 0.0013888888888879082,
-                                        0.04166666666666668, 0.5};
-static __constant__ double c_expO[6] = {2.5110037605963777e-08, 2.755724091857897e-06,
-                                        0.00019841269890047113, 0.008333333333319601,
-                                        0.1666666666666668, 1.0};
+// coefficients (50-digit check): sin(r)/r 1.3e-17 and cos(r) 7.2e-18 on |r| <= pi/4.
+// (cosh/sinh: masw_exp_table.h.)
 static __constant__ double c_sin[6] = {1.5894736651849094e-10, -2.5050716974102745e-08,
                                        2.755731337640013e-06, -0.000198412698286503,
                                        0.008333333333320363, -0.16666666666666616};
@@ -93,40 +89,75 @@ constexpr double kShifter = 6755399441055744.0;         // 1.5 * 2^52: round-to-
 // Split constants whose leading part has <= 21 significant bits (low word zero), so the
 // leading part is an instruction immediate (no register materialisation) and n * part is
 // exact for the n that occur; the trailing parts come from the constant bank (c_k).
-constexpr double kLn2Hi = 0.6931471824645996;           // ln 2 = kLn2Hi + c_k[1] (+1.7e-25)
 constexpr double kPio2Hi = 1.570796012878418;           // pi/2 = kPio2Hi + c_k[3] + c_k[4]
 static __constant__ double c_k[6] = {
-    1.4426950408889634,        // 0: log2 e
-    -1.904654299957768e-09,    // 1: ln 2 - kLn2Hi
+    kExpInvD,                  // 0: 8 / ln 2 (cosh/sinh reduction step d = ln2/8)
+    kExpD_lo,                  // 1: d - kExpD_hi
     0.6366197723675814,        // 2: 2 / pi
     3.139164786504813e-07,     // 3: pi/2 - kPio2Hi (53 bits)
     1.0562999066987428e-23,    // 4: the rest (residual 5e-40)
     0.375,                     // 5: rsqrt correction coefficient
 };
 
-// 2^(n-1), 2^(-n-1) and their sum and difference (rounded as fp64 addition rounds them) for
-// the cosh/sinh reconstruction, n = 0..511 (th = n ln2 + r <= 350 gives n <= 505): a
-// per-CTA table at the start of the kernel's dynamic shared memory (16 KB), read with two
-// 128-bit loads -- lanes of a warp hold neighbouring velocities, so their n mostly coincide
-// (broadcast).  Filled by exp_scale_fill() at kernel start.
-struct __align__(16) ExpScale {
-    double a, b, apb, amb;
-};
-constexpr int kExpTab = 512;
-constexpr unsigned kExpTabBytes = kExpTab * sizeof(ExpScale);
+// cosh/sinh reconstruction table (masw_exp_table.h, generated, correctly rounded): a
+// per-CTA copy at the start of the kernel's dynamic shared memory, filled by
+// exp_scale_fill() at kernel start -- (cosh(m d), sinh(m d)) for m < 512 (8 KB) and 2^(j/8)
+// for j < 8.  Lanes of a warp hold neighbouring velocities, so their m mostly coincide
+// (broadcast reads).
+constexpr unsigned kExpTabBytes = kExpTabN * 16u + 8u * 8u;
 
-__device__ __forceinline__ void exp_scale_fill(ExpScale *tab)
+__device__ __forceinline__ void exp_scale_fill(void *tab)
 {
-    for (int n = threadIdx.x; n < kExpTab; n += blockDim.x) {
-        const double a = __hiloint2double((n + 1022) << 20, 0);
-        const double b = __hiloint2double((1022 - n) << 20, 0);
-        ExpScale e;
-        e.a = a;
-        e.b = b;
-        e.apb = a + b;
-        e.amb = a - b;
-        tab[n] = e;
-    }
+    double2 *t2 = reinterpret_cast<double2 *>(tab);
+    for (int m = threadIdx.x; m < kExpTabN; m += blockDim.x) t2[m] = g_cosh_sinh[m];
+    double *t1 = reinterpret_cast<double *>(t2 + kExpTabN);
+    if (threadIdx.x < 8) t1[threadIdx.x] = g_exp2_8[threadIdx.x];
+}
+
+// Shared-memory addressing with 32-bit shared-window addresses held in registers.  The
+// compiler otherwise re-derives the (cluster-qualified) shared address of a table or a
+// per-warp array from special registers and the launch parameters at every use inside the
+// hot loop (measured: ~25 integer instructions per node in the model-major kernel).
+// opaque() hides a value's origin so it stays in a register; its memory clobber also orders
+// the loads below after the stores that filled the memory.
+__device__ __forceinline__ unsigned smem_addr(const void *p)
+{
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned opaque(unsigned x)
+{
+    asm volatile("" : "+r"(x) : : "memory");
+    return x;
+}
+__device__ __forceinline__ double2 lds_v2(unsigned a)
+{
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned a)
+{
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s32(unsigned a)
+{
+    int v;
+    asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ LayerConst load_lc_at(unsigned a)
+{
+    const double2 p = lds_v2(a), q = lds_v2(a + 16), r = lds_v2(a + 32);
+    LayerConst L;
+    L.kh = p.x;
+    L.ia2 = p.y;
+    L.ib2 = q.x;
+    L.krho = q.y;
+    L.mu = r.x;
+    L.pad = r.y;
+    return L;
 }
 
 // The MUFU fp64 seeds (rcp.approx.ftz.f64, rsqrt.approx.ftz.f64) have relative error
@@ -168,34 +199,41 @@ __device__ __forceinline__ double scale2(double x, int k)
     return __hiloint2double(__double2hiint(x) + (k << 20), __double2loint(x));
 }
 
-// cosh and sinh of th in [0, 700] without branches (the caller guarantees th <= 350, range
-// guard S9).  th = n ln2 + r, |r| <= ln2/2; e^r - 1 is split into its even part
-// E = r^2/2! + r^4/4! + ... and odd part O = r + r^3/3! + ... (two independent Horner
-// chains in r^2, near-minimax degree 5), so e^r - 1 = E + O and e^-r - 1 = E - O need no
-// reciprocal.  With a = 2^(n-1), b = 2^(-n-1):
-//   cosh = (a + b) + a (E + O) + b (E - O)
-//   sinh = (a - b) + a (E + O) - b (E - O)   (= O exactly structured at n = 0: no cancellation)
-__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh,
-                                          const ExpScale *__restrict__ tab)
+// cosh and sinh of th in [0, 350] (the range guard S9 bounds k h_e by 350 and x <= 1).
+// th = m d + r with d = ln2/8, |r| <= ln2/16; with A = cosh(m d), B = sinh(m d) from the
+// table and E = cosh r - 1, O = sinh r (near-minimax degree-3 polynomials in r^2, rel. err
+// < 6e-19):
+//   cosh th = A (1 + E) + B O,   sinh th = B (1 + E) + A O.
+// At m = 0 (A = 1, B = 0) sinh th = O exactly structured (no cancellation at small th); for
+// m >= 1, B and A O do not cancel (th >= m d / 2).  For m >= 512 (th > 44.4) A = B =
+// 2^(n-1) 2^(j/8) (m = 8n + j) to fp64 precision.
+__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, unsigned tab)
 {
     const double t = fma(th, c_k[0], kShifter);
-    const double nd = t - kShifter;
-    const int n = __double2loint(t);
-    double r = fma(nd, -kLn2Hi, th);
-    r = fma(nd, -c_k[1], r);
-    const double r2 = r * r;
-    double pe = c_expE[0];                     // E / r^2  (~ 1/2! + r^2/4! + ...)
-    double po = c_expO[0];                     // O / r    (~ 1 + r^2/3! + ...)
+    const double md = t - kShifter;
+    const unsigned m = (unsigned)__double2loint(t);
+    double r = fma(md, -kExpD_hi, th);                     // exact (m kExpD_hi has <= 33 bits)
+    r = fma(md, -c_k[1], r);
+    const double u = r * r;
+    double pe = c_expE3[0];                                // E / r^2
+    double po = c_expO3[0];                                // O / r
 #pragma unroll
-    for (int i = 1; i < 6; ++i) {
-        pe = fma(pe, r2, c_expE[i]);
-        po = fma(po, r2, c_expO[i]);
+    for (int i = 1; i < 4; ++i) {
+        pe = fma(pe, u, c_expE3[i]);
+        po = fma(po, u, c_expO3[i]);
     }
-    const double E = pe * r2, O = po * r;
-    const ExpScale S = tab[n & (kExpTab - 1)];
-    const double ep = E + O, em = E - O;                       // e^r - 1, e^-r - 1
-    ch = fma(S.a, ep, fma(S.b, em, S.apb));
-    sh = fma(S.a, ep, fma(-S.b, em, S.amb));
+    const double E = pe * u, O = po * r;
+    double A, B;
+    if (m < (unsigned)kExpTabN) {
+        const double2 ab = lds_v2(tab + m * 16u);
+        A = ab.x;
+        B = ab.y;
+    } else {
+        A = scale2(lds_f64(tab + (unsigned)kExpTabN * 16u + (m & 7u) * 8u), (int)(m >> 3) - 1);
+        B = A;
+    }
+    ch = fma(A, E, fma(B, O, A));
+    sh = fma(B, E, fma(A, O, B));
 }
 
 // sin and cos of th in [0, 8e5] (< 2^19 pi/2: 3-part Cody-Waite reduction, the first product
@@ -267,7 +305,7 @@ __device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, dou
 // -------------------------------------------------------------- wave triples
 // (C, XS, SX) of one wave: q = 1 - c^2/v^2 (!= 0 by S4) and kh = k*h; see header comment.
 __device__ __forceinline__ void wave_hyp(double q, double kh, double &C, double &XS, double &SX,
-                                         const ExpScale *__restrict__ tab)
+                                         unsigned tab)
 {
     double x, rq;                      // x, 1/x
     sqrt_rsqrt(q, x, rq);
@@ -295,7 +333,7 @@ __device__ __forceinline__ void wave_trig(double q, double kh, double &C, double
 }
 
 __device__ __forceinline__ void wave_triple(double q, double kh, double &C, double &XS,
-                                            double &SX, const ExpScale *__restrict__ tab)
+                                            double &SX, unsigned tab)
 {
     if (q > 0.0) {
         wave_hyp(q, kh, C, XS, SX, tab);
@@ -353,14 +391,14 @@ __device__ __forceinline__ Elem elem_from_triples(double Cr, double XSr, double 
 // Rare case c > alpha_e (both waves possibly trigonometric): kept out of line so the hot
 // loop's code stays small (instruction-cache pressure was measured: no_instruction stalls).
 static __device__ __noinline__ void waves_general(double qa, double qb, double kh, double *t,
-                                                  const ExpScale *tab)
+                                                  unsigned tab)
 {
     wave_triple(qa, kh, t[0], t[1], t[2], tab);
     wave_triple(qb, kh, t[3], t[4], t[5], tab);
 }
 
 __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
-                                           const ExpScale *__restrict__ tab)
+                                           unsigned tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
     const double qb = fma(-c2, L.ib2, 1.0);   // s^2
@@ -401,7 +439,7 @@ __device__ __forceinline__ double2 wave_root(double q)
 
 __device__ __forceinline__ void wave_hyp_root(double x, double rx, double kh, double &C,
                                               double &XS, double &SX,
-                                              const ExpScale *__restrict__ tab)
+                                              unsigned tab)
 {
     double ch, sh;
     cosh_sinh(kh * x, ch, sh, tab);
@@ -431,7 +469,7 @@ __device__ __forceinline__ void wave_trig_root(double xneg, double rx, double kh
 // mu = (k rho) beta^2 are formed here exactly as the row scan's LayerConst fill forms them).
 __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, double2 a,
                                                 double2 b, double c2,
-                                                const ExpScale *__restrict__ tab)
+                                                unsigned tab)
 {
     const double kh = k * M.kh;
     const double krho = k * M.krho;
@@ -793,7 +831,7 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
 template <bool WANT_VALUE, int NFIX = 0>
 __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
                                         const double *__restrict__ vel,
-                                        const ExpScale *__restrict__ tab, int Nrt, double c,
+                                        unsigned tab, int Nrt, double c,
                                         bool maybe_near = true)
 {
     const int N = NFIX > 0 ? NFIX : Nrt;

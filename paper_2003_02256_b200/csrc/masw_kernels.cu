@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     const int team = warp / TEAM, wt = warp % TEAM, tl = wt * 32 + lane;
 
     // dynamic shared memory: [cosh/sinh scale table | team controls | per-team row constants]
-    ExpScale *tab = reinterpret_cast<ExpScale *>(smem);
+    unsigned char *tab = smem;
     TeamCtrl *ctrl = reinterpret_cast<TeamCtrl *>(smem + kExpTabBytes) + team;
     const unsigned moff = kExpTabBytes + round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
                           (unsigned)team * team_model_bytes(N);
@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     }
     __syncthreads();
     if (s_abort) return;
+    const unsigned ta = opaque(smem_addr(tab));
 
     const int64_t M = a.mod.M, L = a.L, V = a.V;
     const int64_t rows = M * L;
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             int s = 0;
             bool bad = false;
             if (j < V) {
-                const DetOut d = det_K<false, NFIX>(lc, vel, tab, N, c, false);
+                const DetOut d = det_K<false, NFIX>(lc, vel, ta, N, c, false);
                 s = d.sign;
                 bad = d.bad;
                 ++my_eval;
@@ -391,13 +392,17 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 // K^ = K / k has the sign of K).
 constexpr int kModelRows = 64;
 
+// Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
+// velocities (S4), k per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
+// number of 16-byte units, so the lanes' 128-bit loads are conflict-free): the roots
+// (x_a, 1/|x_a|), (x_b, 1/|x_b|) of every layer, the half-space (r, s), (gw, t) and case.
+__host__ __device__ inline unsigned lane_cache_stride(int N) { return 32u * (unsigned)N + 48u; }
 __host__ __device__ inline unsigned warp_model_bytes(int N)
 {
     return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
                    2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
                    (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
-                   2u * (unsigned)N * 32u * 16u +                          // roots P, S [e][lane]
-                   2u * 32u * 16u + 32u * 4u);                             // half-space, case
+                   32u * lane_cache_stride(N));                            // per-lane roots
 }
 
 __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanArgs a)
@@ -407,15 +412,13 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
 
     const int N = a.mod.N;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    ExpScale *tab = reinterpret_cast<ExpScale *>(smem);
+    unsigned char *tab = smem;
     unsigned char *wb = smem + kExpTabBytes + (unsigned)warp * warp_model_bytes(N);
     LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
     double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
     double *kr = vel + 2 * (N + 1);
-    double2 *RA = reinterpret_cast<double2 *>(kr + kModelRows);   // P-wave roots [e][lane]
-    double2 *RB = RA + 32 * N;                                     // S-wave roots [e][lane]
-    double2 *HS = RB + 32 * N;                                     // half-space [2][lane]
-    int *HK = reinterpret_cast<int *>(HS + 64);                    // half-space case [lane]
+    const unsigned stride = lane_cache_stride(N);
+    unsigned char *cl = reinterpret_cast<unsigned char *>(kr + kModelRows) + (unsigned)lane * stride;
 
     Workspace *ws = a.ws;
     exp_scale_fill(tab);
@@ -426,6 +429,7 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
     }
     __syncthreads();
     if (s_abort) return;
+    const unsigned ta = opaque(smem_addr(tab));
 
     const int64_t M = a.mod.M, L = a.L, V = a.V;
     const int64_t groups = (L + kModelRows - 1) / kModelRows;
@@ -462,6 +466,8 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
         }
         for (int r = lane; r < nr; r += 32) kr[r] = kTwoPi / a.lam[i0 + r];   // reading S2
         __syncwarp();
+        const unsigned ma = opaque(smem_addr(mc));
+        const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
 
         const unsigned long long all = (nr == 64) ? ~0ull : ((1ull << nr) - 1ull);
         unsigned long long done = 0, cpos = 0, cneg = 0;   // per row: found, carry sign
@@ -486,19 +492,21 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
             }
             const double c2 = c * c;
             // wavelength-free terms of this lane's velocity (lane-private slots: no sync)
-            for (int e = 0; e < N; ++e) {
-                const LayerConst Lc = load_lc(mc + e);
-                RA[e * 32 + lane] = wave_root(fma(-c2, Lc.ia2, 1.0));
-                RB[e * 32 + lane] = wave_root(fma(-c2, Lc.ib2, 1.0));
-            }
             {
-                const LayerConst Hl = load_lc(mc + N);
+                double2 *rt = reinterpret_cast<double2 *>(cl);
+                for (int e = 0; e < N; ++e) {
+                    const LayerConst Lc = mc[e];
+                    rt[2 * e] = wave_root(fma(-c2, Lc.ia2, 1.0));
+                    rt[2 * e + 1] = wave_root(fma(-c2, Lc.ib2, 1.0));
+                }
+                const LayerConst Hl = mc[N];
                 const HsRoot h = halfspace_root(Hl.ia2, Hl.ib2, c2);
-                HS[lane] = make_double2(h.r, h.s);
-                HS[32 + lane] = make_double2(h.gw, h.t);
-                HK[lane] = h.kase;
+                rt[2 * N] = make_double2(h.r, h.s);
+                rt[2 * N + 1] = make_double2(h.gw, h.t);
+                *reinterpret_cast<int *>(rt + 2 * N + 2) = h.kase;
             }
-            const LayerConst Hl = load_lc(mc + N);
+            const unsigned ca = opaque(smem_addr(cl));
+            const unsigned hca = ca + 32u * (unsigned)N;
             for (unsigned long long pend = all & ~done; pend; pend &= pend - 1) {
                 const int r = __ffsll((long long)pend) - 1;
                 const double k = kr[r];
@@ -508,18 +516,20 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
                     const DetOut d = det_core<false, 0>(
                         N,
                         [&](int e) {
-                            return layer_elem_root(load_lc(mc + e), k, RA[e * 32 + lane],
-                                                   RB[e * 32 + lane], c2, tab);
+                            const unsigned o = 32u * (unsigned)e;
+                            return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
+                                                   lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
                         },
                         [&] {
-                            const double2 rs = HS[lane], gt = HS[32 + lane];
+                            const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
+                            const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
                             HsRoot h;
                             h.r = rs.x;
                             h.s = rs.y;
                             h.gw = gt.x;
                             h.t = gt.y;
-                            h.kase = HK[lane];
-                            return halfspace_k(h, (k * Hl.krho) * Hl.mu);
+                            h.kase = lds_s32(hca + 32u);
+                            return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
                         });
                     s = d.sign;
                     bad = d.bad;
@@ -551,6 +561,7 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
                     cneg = (cneg & ~(1ull << r)) | ((unsigned long long)(last < 0) << r);
                 }
             }
+            __syncwarp();   // the next chunk rewrites this lane's roots
         }
         for (unsigned long long pend = all & ~done; pend; pend &= pend - 1) {
             const int r = __ffsll((long long)pend) - 1;
@@ -869,7 +880,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (ws_invalid(ws, 0x1Fu, true)) return;
-    ExpScale *tab = reinterpret_cast<ExpScale *>(smem);
+    unsigned char *tab = smem;
     exp_scale_fill(tab);
     const int N = mod.N;
     LayerConst *lc = reinterpret_cast<LayerConst *>(smem + kExpTabBytes);
@@ -892,7 +903,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
     __syncthreads();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
-    const DetOut d = det_K<true>(lc, vel, tab, N, c[j]);
+    const DetOut d = det_K<true>(lc, vel, smem_addr(tab), N, c[j]);
     const int64_t o = i * V + j;
     mre[o] = d.mre;
     mim[o] = d.mim;
