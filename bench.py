@@ -365,10 +365,12 @@ def run_ours(args):
     achieved = my_dets_per_step * F / (kern_ms / 1e3) / 1e12
     peak = fp64_peak_tflops()
     traffic, hw = None, {}
+    kern_name = "scan_models_kernel"
     prof = os.path.join(ROOT, "profiles", "scan_kernel_ncu.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
+            kern_name = pj.get("kernel", kern_name)
             # captured on the bench's own scan launch (same workload): bytes per launch
             traffic = pj.get("dram_bytes")
             hw = {"fp64_pipe_pct_active": pj.get("fp64_pipe_pct_active"),
@@ -396,7 +398,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches / args.steps,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "scan_kernel<1,256> (fused assemble + banded GEPP det + ballot scan)",
+                     "kernel": kern_name + " (fused assemble + banded GEPP det + ballot scan)",
                      "kernel_ms": kern_ms, "flops_per_det": F,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
                                     "(B200_PROFILING.md counts; MEASURED_PEAKS.json has no FP64)",

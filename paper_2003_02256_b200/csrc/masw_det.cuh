@@ -497,6 +497,7 @@ __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, d
 // the case) and the mu-dependent entries.
 struct HalfSpace {
     double h11r, h11i, h12r, h12i, h22r, h22i;
+    bool real;   // all imaginary parts zero (c < beta_N)
 };
 struct HsRoot {
     double r, s, gw, t;
@@ -533,6 +534,7 @@ __device__ __forceinline__ HsRoot halfspace_root(double ia2, double ib2, double 
 __device__ __forceinline__ HalfSpace halfspace_k(const HsRoot &R, double mu)
 {
     HalfSpace H;
+    H.real = R.kase == 0;
     if (R.kase == 0) {
         const double g = mu * R.gw;
         H.h11r = R.r * g; H.h11i = 0.0;
@@ -623,7 +625,7 @@ __device__ __forceinline__ void gepp_finish(double (&R)[4][NC], double (&Ri)[4][
     constexpr int lo = (Q == 2) ? pos1 : pos2;
     constexpr int hi = (Q == 3) ? pos1 : pos3;
     o.piv1 = R[prow][1];
-    const double inv1 = o.key1 ? rcp_fast(o.piv1) : 0.0;
+    const double inv1 = rcp_fast(o.piv1);
     const double l_lo = R[lo][1] * inv1, l_hi = R[hi][1] * inv1;
     // zero pattern after the column-0 elimination (rows != P)
     constexpr auto zr = [](int i, int c) { return zre0<NC, NR>(i, c) && zre0<NC, NR>(P, c); };
@@ -654,7 +656,7 @@ __device__ __forceinline__ void gepp_after_p(double (&R)[4][NC], double (&Ri)[4]
                                              double (&Xi)[2][NC - 2])
 {
     o.piv0 = R[P][0];
-    const double inv0 = o.key0 ? rcp_fast(o.piv0) : 0.0;
+    const double inv0 = rcp_fast(o.piv0);
     // eliminate column 0 from the three other rows with pivot row P (skipping the pivot
     // row's known zeros)
 #pragma unroll
@@ -769,17 +771,37 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
 
     const HalfSpace H = hs();
 
-    // Last step: node N-1 columns real, node N columns complex (NR = 2).
-    double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
-                      {X[1][0], X[1][1], X[1][2], X[1][3]},
-                      {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
-                      {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
-    double Ri[4][4] = {{0.0, 0.0, 0.0, 0.0},
-                       {0.0, 0.0, 0.0, 0.0},
-                       {0.0, 0.0, H.h11i, H.h12i},
-                       {0.0, 0.0, H.h12i, H.h22i}};
-    double Y[2][2], Yi[2][2];
-    const StepOut so = gepp_step<4, 2>(R, Ri, Y, Yi);
+    // Last step: node N-1 columns real, node N columns complex (NR = 2) -- or real when
+    // c < beta_N (K_hs real, the common case below the half-space shear velocity).
+    double dre, dim;
+    StepOut so;
+    if (H.real) {
+        double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
+                          {X[1][0], X[1][1], X[1][2], X[1][3]},
+                          {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
+                          {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
+        double Ri[4][4];   // unused: NR = 0
+        double Y[2][2], Yi[2][2];
+        so = gepp_step<4, 0>(R, Ri, Y, Yi);
+        dre = fma(Y[0][0], Y[1][1], -Y[0][1] * Y[1][0]);
+        dim = 0.0;
+    } else {
+        double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
+                          {X[1][0], X[1][1], X[1][2], X[1][3]},
+                          {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
+                          {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
+        double Ri[4][4] = {{0.0, 0.0, 0.0, 0.0},
+                           {0.0, 0.0, 0.0, 0.0},
+                           {0.0, 0.0, H.h11i, H.h12i},
+                           {0.0, 0.0, H.h12i, H.h22i}};
+        double Y[2][2], Yi[2][2];
+        so = gepp_step<4, 2>(R, Ri, Y, Yi);
+        // det of the last complex 2x2
+        dre = fma(Y[0][0], Y[1][1], -Yi[0][0] * Yi[1][1]) -
+              fma(Y[0][1], Y[1][0], -Yi[0][1] * Yi[1][0]);
+        dim = fma(Y[0][0], Yi[1][1], Yi[0][0] * Y[1][1]) -
+              fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
+    }
     sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
     kmin = min(kmin, min(so.key0, so.key1));
     kmax = max(kmax, max(so.key0, so.key1));
@@ -788,14 +810,13 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
         acc.mul(so.piv0);
         acc.mul(so.piv1);
     }
-    // det of the last complex 2x2
-    const double dre = fma(Y[0][0], Y[1][1], -Yi[0][0] * Yi[1][1]) -
-                       fma(Y[0][1], Y[1][0], -Yi[0][1] * Yi[1][0]);
-    const double dim = fma(Y[0][0], Yi[1][1], Yi[0][0] * Y[1][1]) -
-                       fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
     kmax = max(kmax, max(mag_key(dre), mag_key(dim)));
-    const bool bad = kmax >= 0x7ff00000;
+    // A zero pivot (key 0: the pivot column is zero, det K = 0 exactly) makes every later
+    // pivot NaN through the unguarded reciprocal; it takes precedence, as in the oracle's
+    // elimination, which stops there with det = 0.  Inputs are finite and the range guard S9
+    // keeps every entry finite, so no Inf/NaN can precede a zero pivot.
     const bool zero = (kmin == 0) || (dre == 0.0);
+    const bool bad = (kmax >= 0x7ff00000) && (kmin != 0);
     const bool neg = (perm != 0) ^ ((sgn >> 31) != 0) ^ (dre < 0.0);
 
     DetOut out;
@@ -804,7 +825,7 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
     out.mre = 0.0;
     out.mim = 0.0;
     out.e2 = 0;
-    if (WANT_VALUE) {
+    if (WANT_VALUE && kmin != 0) {
         // value = (-1)^permutation * (prod pivots) * (dre + i dim)
         const double ps = perm ? -acc.m : acc.m;
         double re = ps * dre, im = ps * dim;
