@@ -100,18 +100,23 @@ static __constant__ double c_k[6] = {
 };
 
 // cosh/sinh reconstruction table (masw_exp_table.h, generated, correctly rounded): a
-// per-CTA copy at the start of the kernel's dynamic shared memory, filled by
-// exp_scale_fill() at kernel start -- (cosh(m d), sinh(m d)) for m < 512 (8 KB) and 2^(j/8)
-// for j < 8.  Lanes of a warp hold neighbouring velocities, so their m mostly coincide
-// (broadcast reads).
-constexpr unsigned kExpTabBytes = kExpTabN * 16u + 8u * 8u;
+// per-CTA copy at the start of the kernel's dynamic shared memory -- (cosh(m d), sinh(m d))
+// for m < 4096, 64 KB, read without a branch.  exp_scale_fill() copies only the rows the
+// launch can reach (m <= kh_max / d + 1, kh_max = max k h over the call's rows and layers,
+// which the range guard S9 bounds by 350).  Lanes of a warp hold neighbouring velocities, so
+// their m mostly coincide (broadcast reads).
+constexpr unsigned kExpTabBytes = kExpTabN * 16u;
 
-__device__ __forceinline__ void exp_scale_fill(void *tab)
+__device__ __forceinline__ int exp_rows_needed(double kh_max)
+{
+    const double m = kh_max * kExpInvD + 2.0;
+    return (m < (double)kExpTabN) ? (int)m : kExpTabN;   // (NaN -> all rows)
+}
+
+__device__ __forceinline__ void exp_scale_fill(void *tab, int rows)
 {
     double2 *t2 = reinterpret_cast<double2 *>(tab);
-    for (int m = threadIdx.x; m < kExpTabN; m += blockDim.x) t2[m] = g_cosh_sinh[m];
-    double *t1 = reinterpret_cast<double *>(t2 + kExpTabN);
-    if (threadIdx.x < 8) t1[threadIdx.x] = g_exp2_8[threadIdx.x];
+    for (int m = threadIdx.x; m < rows; m += blockDim.x) t2[m] = g_cosh_sinh[m];
 }
 
 // Shared-memory addressing with 32-bit shared-window addresses held in registers.  The
@@ -205,8 +210,7 @@ __device__ __forceinline__ double scale2(double x, int k)
 // < 6e-19):
 //   cosh th = A (1 + E) + B O,   sinh th = B (1 + E) + A O.
 // At m = 0 (A = 1, B = 0) sinh th = O exactly structured (no cancellation at small th); for
-// m >= 1, B and A O do not cancel (th >= m d / 2).  For m >= 512 (th > 44.4) A = B =
-// 2^(n-1) 2^(j/8) (m = 8n + j) to fp64 precision.
+// m >= 1, B and A O do not cancel (th >= m d / 2).
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, unsigned tab)
 {
     const double t = fma(th, c_k[0], kShifter);
@@ -223,15 +227,8 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, uns
         po = fma(po, u, c_expO3[i]);
     }
     const double E = pe * u, O = po * r;
-    double A, B;
-    if (m < (unsigned)kExpTabN) {
-        const double2 ab = lds_v2(tab + m * 16u);
-        A = ab.x;
-        B = ab.y;
-    } else {
-        A = scale2(lds_f64(tab + (unsigned)kExpTabN * 16u + (m & 7u) * 8u), (int)(m >> 3) - 1);
-        B = A;
-    }
+    const double2 ab = lds_v2(tab + (m & (unsigned)(kExpTabN - 1)) * 16u);
+    const double A = ab.x, B = ab.y;
     ch = fma(A, E, fma(B, O, A));
     sh = fma(B, E, fma(A, O, B));
 }

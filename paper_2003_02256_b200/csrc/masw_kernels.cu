@@ -51,6 +51,14 @@ __device__ __forceinline__ bool ws_range_bad(const Workspace *ws)
     return kmax * h_max > kMaxKH;
 }
 
+// max over the call's rows and layers of k h_e (validated: <= 350) -> cosh/sinh table rows.
+__device__ __forceinline__ int ws_exp_rows(const Workspace *ws)
+{
+    const double lam_min = __longlong_as_double((long long)~ws->lam_min_nbits);
+    const double h_max = __longlong_as_double((long long)ws->h_max_bits);
+    return exp_rows_needed((kTwoPi / lam_min) * h_max);
+}
+
 // grid_mask selects which grid_err bits make the call invalid.
 __device__ __forceinline__ bool ws_invalid(const Workspace *ws, unsigned grid_mask,
                                            bool check_models)
@@ -212,7 +220,6 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     double *vel = reinterpret_cast<double *>(smem + moff + (unsigned)(N + 1) * sizeof(LayerConst));
 
     Workspace *ws = a.ws;
-    exp_scale_fill(tab);
     if (threadIdx.x == 0) {
         const bool bad = ws_invalid(ws, a.grid_mask, true);
         s_abort = bad;
@@ -220,6 +227,8 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     }
     __syncthreads();
     if (s_abort) return;
+    exp_scale_fill(tab, ws_exp_rows(ws));
+    __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
 
     const int64_t M = a.mod.M, L = a.L, V = a.V;
@@ -391,6 +400,8 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 // only its k h_e-dependent part.  Results are those of scan_kernel (same algorithm per row,
 // K^ = K / k has the sign of K).
 constexpr int kModelRows = 64;
+// 16 warps in ONE CTA per SM: one copy of the 64 KB cosh/sinh table serves all of them.
+constexpr int kModelsBlock = 512;
 
 // Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
 // velocities (S4), k per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
@@ -405,7 +416,7 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
                    32u * lane_cache_stride(N));                            // per-lane roots
 }
 
-__global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanArgs a)
+__global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_abort;
@@ -421,7 +432,6 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
     unsigned char *cl = reinterpret_cast<unsigned char *>(kr + kModelRows) + (unsigned)lane * stride;
 
     Workspace *ws = a.ws;
-    exp_scale_fill(tab);
     if (threadIdx.x == 0) {
         const bool bad = ws_invalid(ws, a.grid_mask, true);
         s_abort = bad;
@@ -429,6 +439,8 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
     }
     __syncthreads();
     if (s_abort) return;
+    exp_scale_fill(tab, ws_exp_rows(ws));
+    __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
 
     const int64_t M = a.mod.M, L = a.L, V = a.V;
@@ -576,7 +588,8 @@ __global__ void __launch_bounds__(256, MASW_SCAN_MINB) scan_models_kernel(ScanAr
         }
         __syncwarp();   // the next item rewrites this warp's constants
     }
-    if (a.team_dets && lane == 0) a.team_dets[(long long)blockIdx.x * 8 + warp] = team_alg;
+    if (a.team_dets && lane == 0)
+        a.team_dets[(long long)blockIdx.x * (kModelsBlock / 32) + warp] = team_alg;
 
     my_alg = warp_sum_u64(my_alg);
     my_eval = warp_sum_u64(my_eval);
@@ -601,6 +614,39 @@ int sm_count(int device)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (device >= 0 && device < 64) g_sms[device] = sms;
     return sms;
+}
+// Opt-in dynamic shared memory: raised ONCE per (device, kernel) to the device maximum, so a
+// later launch never runs with a limit left lower by an earlier, smaller launch (the limit
+// does not enter the occupancy computation, which takes the launch's own size).
+std::unordered_map<long long, bool> g_smem_set;
+
+template <class K>
+cudaError_t ensure_smem_optin(K kern, int device, int kid)
+{
+    const long long key = ((long long)device << 8) | kid;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        if (g_smem_set.count(key)) return cudaSuccess;
+    }
+    int optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    g_smem_set[key] = true;
+    return cudaSuccess;
+}
+
+size_t smem_optin_limit(int device)
+{
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    return (size_t)optin;
 }
 }  // namespace
 
@@ -636,12 +682,11 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
         auto it = g_occ_cache.find(key);
         if (it != g_occ_cache.end()) per_sm = it->second;
     }
+    {
+        cudaError_t e = ensure_smem_optin(kern, device, 16 + TEAM);
+        if (e != cudaSuccess) return e;
+    }
     if (per_sm == 0) {
-        if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(
-                kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-        }
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) per_sm = 1;
@@ -692,7 +737,10 @@ long long scan_teams(const ScanArgs &a, int team_warps, int device)
 }
 
 // Model-major launch: one work item per (model, block of kModelRows wavelengths).
-static size_t models_smem(int N) { return kExpTabBytes + 8u * (size_t)warp_model_bytes(N); }
+static size_t models_smem(int N)
+{
+    return kExpTabBytes + (size_t)(kModelsBlock / 32) * (size_t)warp_model_bytes(N);
+}
 
 static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
                                  long long *warps_out, bool dry, int *per_sm_out = nullptr)
@@ -710,19 +758,15 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
     if (per_sm == 0) {
         // a cache that does not fit is "0 CTAs per SM", not an error (and must not leave a
         // pending runtime error for the next launch's cudaGetLastError)
-        int optin = 0;
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         const size_t static_smem = 16;
-        if (smem + static_smem > (size_t)optin) {
+        if (smem + static_smem > smem_optin_limit(device)) {
             per_sm = -1;
         } else {
-            if (smem > 48 * 1024 &&
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem) != cudaSuccess) {
+            if (ensure_smem_optin(kern, device, 1) != cudaSuccess) {
                 cudaGetLastError();
                 per_sm = -1;
-            } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) !=
-                       cudaSuccess) {
+            } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kModelsBlock,
+                                                                     smem) != cudaSuccess) {
                 cudaGetLastError();
                 per_sm = -1;
             }
@@ -736,21 +780,21 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
     if (per_sm == 0) return cudaErrorInvalidConfiguration;
     const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
     int64_t blocks = (int64_t)sms * per_sm;
-    const int64_t need = (items + 7) / 8;
+    const int64_t need = (items + kModelsBlock / 32 - 1) / (kModelsBlock / 32);
     if (need < blocks) blocks = need;
     if (blocks < 1) blocks = 1;
-    if (warps_out) *warps_out = blocks * 8;
+    if (warps_out) *warps_out = blocks * (kModelsBlock / 32);
     if (dry) return cudaSuccess;
-    kern<<<(unsigned)blocks, 256, smem, st>>>(a);
+    kern<<<(unsigned)blocks, kModelsBlock, smem, st>>>(a);
     count_launch();
     return cudaGetLastError();
 }
 
 bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
 {
-    // unless forced: enough work items to fill the GPU several times over, several
-    // wavelengths per model to share the cache, and two 256-thread CTAs per SM with the
-    // per-warp caches (N <= ~8)
+    // unless forced: enough work items to fill the GPU several times over and several
+    // wavelengths per model to share the cache; and one 16-warp CTA per SM with the table
+    // and the per-warp caches must fit (N <= 7)
     const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
     const int sms = sm_count(device);
     if (a.sched != 0) return false;
@@ -758,7 +802,7 @@ bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
     int per_sm = 0;
     long long w = 0;
     if (launch_models(a, nullptr, device, &w, true, &per_sm) != cudaSuccess) return false;
-    return per_sm >= (forced ? 1 : 2);
+    return per_sm >= 1;
 }
 
 cudaError_t launch_scan_models(const ScanArgs &a, cudaStream_t st, int device,
@@ -881,7 +925,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
     extern __shared__ __align__(16) unsigned char smem[];
     if (ws_invalid(ws, 0x1Fu, true)) return;
     unsigned char *tab = smem;
-    exp_scale_fill(tab);
+    exp_scale_fill(tab, ws_exp_rows(ws));
     const int N = mod.N;
     LayerConst *lc = reinterpret_cast<LayerConst *>(smem + kExpTabBytes);
     double *vel = reinterpret_cast<double *>(smem + kExpTabBytes + (size_t)(N + 1) * sizeof(LayerConst));
@@ -915,6 +959,10 @@ cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, co
                             cudaStream_t st)
 {
     const size_t smem = kExpTabBytes + team_model_bytes(m.N);
+    int dev = 0;
+    cudaGetDevice(&dev);   // the C-ABI's DeviceScope has made the call's device current
+    cudaError_t e = ensure_smem_optin(det_grid_kernel, dev, 2);
+    if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((V + 255) / 256), (unsigned)L);
     det_grid_kernel<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws);
     count_launch();

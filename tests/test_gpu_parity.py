@@ -115,6 +115,21 @@ def test_curve_parity_small(masw, orc, name, team):
     assert alg == int(ond.sum()) and ev >= alg          # SPEC.md:246 early-exit count
 
 
+@pytest.mark.parametrize("team", [1, 8, 16])
+def test_alternating_shared_memory_sizes(masw, team):
+    """Launches whose dynamic shared memory shrinks and grows again (different N, same team
+    size): the opt-in limit is raised once per kernel, never left below a later launch."""
+    rng = np.random.default_rng(11)
+    lam = synth.geom(30.0, 2.0, 8)
+    c = 20.0 + 0.5 * np.arange(700, dtype=np.float64)
+    for N in (5, 2, 5, 24, 2, 40):
+        h = rng.uniform(0.5, 2.0, N)
+        beta = rng.uniform(100.0, 400.0, N + 1)
+        st, ct, idx = masw.masw_curve(h, np.full(N + 1, 1440.0), beta, np.full(N + 1, 1900.0),
+                                      lam, c, team_warps=team)
+        assert st in (0, 1)
+
+
 def test_curve_device_pointers_and_async(masw, orc):
     w = synth.workload("maswaves")
     a = margs(w.models)
