@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 // shared memory, and reuses them for every active row -- each row's determinant then needs
 // only its k h_e-dependent part.  Results are those of scan_kernel (same algorithm per row,
 // K^ = K / k has the sign of K).
+#ifndef MASW_MODELS_UNROLL
+#define MASW_MODELS_UNROLL 2
+#endif
 constexpr int kModelRows = 64;
 // 16 warps in ONE CTA per SM: one copy of the 64 KB cosh/sinh table serves all of them.
 constexpr int kModelsBlock = 512;
@@ -525,7 +528,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                 int s = 0;
                 bool bad = false;
                 if (valid) {
-                    const DetOut d = det_core<false, 0>(
+                    const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
                         N,
                         [&](int e) {
                             const unsigned o = 32u * (unsigned)e;
