@@ -673,13 +673,15 @@ __device__ __forceinline__ void gepp_after_p(double (&R)[4][NC], double (&Ri)[4]
     constexpr int pos2 = (P == 2) ? 0 : 2;
     constexpr int pos3 = (P == 3) ? 0 : 3;
     const int b1 = mag_key(R[pos1][1]), b2 = mag_key(R[pos2][1]), b3 = mag_key(R[pos3][1]);
-    o.key1 = max(b1, max(b2, b3));
-    if (b2 > b1 && b2 >= b3) {
-        gepp_finish<NC, NR, P, 2>(R, Ri, o, X, Xi);
-    } else if (b3 > b1 && b3 > b2) {
-        gepp_finish<NC, NR, P, 3>(R, Ri, o, X, Xi);
-    } else {
+    const int b23 = max(b2, b3);
+    o.key1 = max(b1, b23);
+    // first maximum in position order; the common no-swap case (position 1) is tested first
+    if (b1 >= b23) {
         gepp_finish<NC, NR, P, 1>(R, Ri, o, X, Xi);
+    } else if (b2 >= b3) {
+        gepp_finish<NC, NR, P, 2>(R, Ri, o, X, Xi);
+    } else {
+        gepp_finish<NC, NR, P, 3>(R, Ri, o, X, Xi);
     }
 }
 
@@ -696,11 +698,15 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
     if (a2 > best) { best = a2; p = 2; }
     if (a3 > best) { best = a3; p = 3; }
     o.key0 = best;
-    switch (p) {
-        case 0: gepp_after_p<NC, NR, 0>(R, Ri, o, X, Xi); break;
-        case 1: gepp_after_p<NC, NR, 1>(R, Ri, o, X, Xi); break;
-        case 2: gepp_after_p<NC, NR, 2>(R, Ri, o, X, Xi); break;
-        default: gepp_after_p<NC, NR, 3>(R, Ri, o, X, Xi); break;
+    // most frequent first (C5, oracle's dense GEPP: p = 0 63 %, 3 24 %, 1 12 %, 2 1 %)
+    if (p == 0) {
+        gepp_after_p<NC, NR, 0>(R, Ri, o, X, Xi);
+    } else if (p == 3) {
+        gepp_after_p<NC, NR, 3>(R, Ri, o, X, Xi);
+    } else if (p == 1) {
+        gepp_after_p<NC, NR, 1>(R, Ri, o, X, Xi);
+    } else {
+        gepp_after_p<NC, NR, 2>(R, Ri, o, X, Xi);
     }
     return o;
 }
@@ -732,7 +738,7 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
     // always picked as a pivot or reaches the last 2x2 through the updates).
     int perm = 0;
     unsigned sgn = 0;
-    int kmin = 0x7fffffff, kmax = 0;
+    unsigned kmin = 0x7fffffffu, kmax = 0u;
     DetAcc acc{1.0, 0};
 
     Elem P = elem(0);
@@ -749,8 +755,8 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
         double Xi[2][4];
         const StepOut so = gepp_step<6, 0>(R, Ri, X, Xi);
         sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
-        kmin = min(kmin, min(so.key0, so.key1));
-        kmax = max(kmax, max(so.key0, so.key1));
+        kmin = min(kmin, min((unsigned)so.key0, (unsigned)so.key1));
+        kmax = max(kmax, max((unsigned)so.key0, (unsigned)so.key1));
         perm ^= so.parity;
         if (WANT_VALUE) {
             acc.mul(so.piv0);
@@ -801,20 +807,20 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
               fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
     }
     sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
-    kmin = min(kmin, min(so.key0, so.key1));
-    kmax = max(kmax, max(so.key0, so.key1));
+    kmin = min(kmin, min((unsigned)so.key0, (unsigned)so.key1));
+    kmax = max(kmax, max((unsigned)so.key0, (unsigned)so.key1));
     perm ^= so.parity;
     if (WANT_VALUE) {
         acc.mul(so.piv0);
         acc.mul(so.piv1);
     }
-    kmax = max(kmax, max(mag_key(dre), mag_key(dim)));
+    kmax = max(kmax, max((unsigned)mag_key(dre), (unsigned)mag_key(dim)));
     // A zero pivot (key 0: the pivot column is zero, det K = 0 exactly) makes every later
     // pivot NaN through the unguarded reciprocal; it takes precedence, as in the oracle's
     // elimination, which stops there with det = 0.  Inputs are finite and the range guard S9
     // keeps every entry finite, so no Inf/NaN can precede a zero pivot.
     const bool zero = (kmin == 0) || (dre == 0.0);
-    const bool bad = (kmax >= 0x7ff00000) && (kmin != 0);
+    const bool bad = (kmax >= 0x7ff00000u) && (kmin != 0u);
     const bool neg = (perm != 0) ^ ((sgn >> 31) != 0) ^ (dre < 0.0);
 
     DetOut out;
