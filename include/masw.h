@@ -40,7 +40,8 @@
  *   MASW_E_GRID      lambda_i <= 0, c_0 <= 0, or c not strictly increasing
  *   MASW_E_NONFINITE / MASW_E_MODEL  the lowest-index model with a NaN/Inf, or violating
  *                    h > 0, rho > 0, beta > 0, alpha > beta
- *   MASW_E_RANGE     (2*pi/lambda_i) * h_e > 350 for some i, e (cosh overflow guard, S9)
+ *   MASW_E_RANGE     (2*pi/lambda_i) * h_e > 350 for some i, e (cosh overflow guard, S9;
+ *                    700 with MASW_STABLE)
  *   then C_e (when given): NaN/Inf -> MASW_E_NONFINITE, C_e <= 0 -> MASW_E_ARG
  */
 #ifndef MASW_H
@@ -110,6 +111,13 @@ typedef struct {
  * (N <= ~8; else the row scan runs).  With MASW_TEAM_STATS a model-major "team" is a warp. */
 #define MASW_SCHED_ROWS 0x20u
 #define MASW_SCHED_MODELS 0x40u
+/* Numerically stable element: the layer
+ * stiffness is evaluated in cancellation-free form for c -> 0 (both waves hyperbolic) and
+ * with exponentially scaled hyperbolic functions, so the range guard becomes
+ * (2*pi/lambda_i) * h_e <= 700 instead of 350 (MASW_E_RANGE above that).  Costs ~1.7x per
+ * element; runs the row scan (never the model-major one).  Applies to masw_curve,
+ * masw_curves_ensemble and masw_det_grid. */
+#define MASW_STABLE 0x80u
 
 /* Execution options; a NULL masw_exec means {device = current, stream = legacy default,
  * team_warps = 0 (auto), flags = 0}. */

@@ -190,7 +190,7 @@ Workspace read_status(const Workspace *ws, cudaStream_t st)
 }
 
 // Error precedence of include/masw.h from the workspace filled by validate_kernel.
-int decode(const Workspace &w, bool with_ce, bool with_models)
+int decode(const Workspace &w, bool with_ce, bool with_models, bool stable = false)
 {
     if (w.grid_err & 3u) return MASW_E_NONFINITE;
     if (w.grid_err & 28u) return MASW_E_GRID;
@@ -204,7 +204,7 @@ int decode(const Workspace &w, bool with_ce, bool with_models)
         memcpy(&lam_min, &lb, 8);
         memcpy(&h_max, &w.h_max_bits, 8);
         const double kmax = kTwoPi / lam_min;
-        if (kmax * h_max > kMaxKH) return MASW_E_RANGE;
+        if (kmax * h_max > (stable ? kMaxKHStable : kMaxKH)) return MASW_E_RANGE;
     }
     if (with_ce) {
         if (w.grid_err & 32u) return MASW_E_NONFINITE;
@@ -266,10 +266,12 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
 
         const int team = ex.team ? ex.team : auto_team_warps(R, V, dev);
         const int sched = (ex.flags & MASW_SCHED_CONTIGUOUS) ? 1 : ((ex.flags & MASW_SCHED_MODULAR) ? 2 : 0);
-        ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws, dce ? 0x7Fu : 0x1Fu, sched, nullptr};
+        const bool stable = (ex.flags & MASW_STABLE) != 0;
+        ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws,
+                    (dce ? 0x7Fu : 0x1Fu) | (stable ? kGridStable : 0u), sched, nullptr, stable};
         // model-major scan for ensembles (auto unless a team size, a static schedule or
         // MASW_SCHED_ROWS is requested; MASW_SCHED_MODELS forces it where it fits)
-        const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 &&
+        const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 && !stable &&
                             (((ex.flags & MASW_SCHED_MODELS) && models_scan_suitable(sa, dev, true)) ||
                              (ex.team == 0 && models_scan_suitable(sa, dev, false)));
         const bool stats = (ex.flags & MASW_TEAM_STATS) != 0 && !(ex.flags & MASW_ASYNC);
@@ -296,11 +298,11 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
             CK(cudaEventRecord(slot[1], st));
             ++t_scan_count;
         }
-        if (dmis) CK(launch_misfit(dct, dce, M, L, dmis, ws, 0x7Fu, true, st));
+        if (dmis) CK(launch_misfit(dct, dce, M, L, dmis, ws, 0x7Fu | (stable ? kGridStable : 0u), true, st));
 
         if (!host && (ex.flags & MASW_ASYNC)) return MASW_OK;
         const Workspace w = read_status(ws, st);
-        const int code = decode(w, dce != nullptr, true);
+        const int code = decode(w, dce != nullptr, true, stable);
         if (code < 0) return code;
         t_last_alg = (long long)w.alg_dets;
         t_last_eval = (long long)w.eval_dets;
@@ -499,10 +501,11 @@ int masw_det_grid(const masw_model *model, const double *lambda, int64_t L, cons
         Workspace *ws = arena.alloc<Workspace>(1);
         CK(cudaMemsetAsync(ws, 0, sizeof(Workspace), st));
         CK(launch_validate(mod, dlam, L, dc, V, nullptr, ws, st));
-        CK(launch_det_grid(mod, dlam, L, dc, V, dre, dim, dex, ws, st));
+        const bool stable = (ex.flags & MASW_STABLE) != 0;
+        CK(launch_det_grid(mod, dlam, L, dc, V, dre, dim, dex, ws, st, stable));
         if (!host && (ex.flags & MASW_ASYNC)) return MASW_OK;
         const Workspace w = read_status(ws, st);
-        const int code = decode(w, false, true);
+        const int code = decode(w, false, true, stable);
         if (code < 0) return code;
         if (host) {
             CK(cudaMemcpyAsync(mant_re, dre, G * 8, cudaMemcpyDeviceToHost, st));
@@ -524,7 +527,7 @@ const char *masw_strerror(int code)
         case MASW_E_ARG: return "MASW_E_ARG: invalid argument";
         case MASW_E_MODEL: return "MASW_E_MODEL: model violates h>0, rho>0, beta>0, alpha>beta";
         case MASW_E_GRID: return "MASW_E_GRID: lambda <= 0, c0 <= 0 or c not strictly increasing";
-        case MASW_E_RANGE: return "MASW_E_RANGE: 2*pi*h/lambda > 350";
+        case MASW_E_RANGE: return "MASW_E_RANGE: 2*pi*h/lambda > 350 (700 with MASW_STABLE)";
         case MASW_E_NONFINITE: return "MASW_E_NONFINITE: NaN/Inf input";
         case MASW_E_CUDA: return "MASW_E_CUDA: CUDA runtime error";
         case MASW_E_NOMEM: return "MASW_E_NOMEM: device allocation failed";

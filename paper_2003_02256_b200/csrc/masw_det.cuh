@@ -419,6 +419,114 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
     return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2);
 }
 
+// -------------------------------------------------------------- stable element (f3)
+// SURVEY.md §8(f) f3, opt-in (MASW_STABLE): an element evaluation without the two fp64
+// failure modes of the direct App. A formulas (readings S9, S15):
+//  * c -> 0 with both waves hyperbolic: D = 2(1 - Cr Cs) + Sr Ss (1/(rs) + rs) and the
+//    entries' brackets are O(c^4) / O(c^2) differences of O(cosh^2) terms.  With
+//    delta = (th_r - th_s)/2 = k h (r - s)/2, r - s = (b - a)/(r + s), w = 1 - rs =
+//    (a + b - ab)/(1 + rs) (a = c^2/alpha^2, b = c^2/beta^2), the exact identities
+//      D = -4 sinh^2(delta) + (w^2/(rs)) Sr Ss,
+//      Cr Cs - rs Sr Ss - 1 = 2 sinh^2(delta) + w Sr Ss,
+//      Cr Ss - rs Sr Cs = -sinh(2 delta) + w Sr Cs,   Sr Cs - rs Cr Ss = sinh(2 delta) + w Cr Ss,
+//      Sr - Ss = 2 cosh(sigma) sinh(delta),  Cs - Cr = -2 sinh(sigma) sinh(delta),
+//    (sigma = th_s + delta) turn every bracket into terms without cancellation at small c;
+//  * thick layers (k h > 350, cosh overflow): every term carries e^(th_r + th_s) (or e^th_r
+//    in the mixed case), so with scaled functions c^ = cosh(x) e^-x, s^ = sinh(x) e^-x and
+//    e^-x the element is evaluated for k h up to 700 (range guard raised under MASW_STABLE).
+// Validated against 50-digit mpmath (tests/test_gpu_stable.py), not the naive oracle.
+constexpr double kMaxKHStable = 700.0;
+constexpr double kExpSplit = 354.0;                      // within the cosh/sinh table
+constexpr double kExpNeg354 = 0x1.381ea37bd35b3p-511;    // e^-354 (correctly rounded)
+
+struct ExpScaled {
+    double c, s, e;   // cosh(x) e^-x, sinh(x) e^-x, e^-x   (x in [0, 700])
+};
+
+__device__ __forceinline__ ExpScaled exp_scaled(double x, unsigned tab)
+{
+    ExpScaled o;
+    if (x <= kExpSplit) {
+        double C, S;
+        cosh_sinh(x, C, S, tab);
+        o.e = rcp_fast(C + S);
+        o.c = C * o.e;
+        o.s = S * o.e;
+    } else {   // e^-2x < 1e-307: c^ = s^ = 1/2 in fp64
+        double C, S;
+        cosh_sinh(x - kExpSplit, C, S, tab);
+        o.e = rcp_fast(C + S) * kExpNeg354;
+        o.c = 0.5;
+        o.s = 0.5;
+    }
+    return o;
+}
+
+// Both waves hyperbolic (c < beta_e < alpha_e); entries as described above, all scaled by
+// e^-(th_r + th_s) in numerator and denominator (f = f^ e^-(th_r + th_s)).
+__device__ __forceinline__ Elem elem_stable_hh(double kh, double c2, double ia2, double ib2,
+                                               double krho, double mu, unsigned tab)
+{
+    const double a = c2 * ia2, b = c2 * ib2;
+    double r, rr, s, rsn;
+    sqrt_rsqrt(1.0 - a, r, rr);
+    sqrt_rsqrt(1.0 - b, s, rsn);
+    const double rs = r * s;
+    const double w = fma(-a, b, a + b) * rcp_fast(1.0 + rs);          // 1 - rs
+    const double dl = 0.5 * kh * ((b - a) * rcp_fast(r + s));          // (th_r - th_s)/2
+    const ExpScaled R = exp_scaled(kh * r, tab), S = exp_scaled(kh * s, tab);
+    const ExpScaled Dl = exp_scaled(dl, tab);
+    const double es2 = S.e * S.e;                                      // e^-2 th_s
+    const double sd2 = Dl.s * Dl.s;
+    const double sdcd2 = 2.0 * Dl.s * Dl.c;
+    const double csig = fma(S.c, Dl.c, S.s * Dl.s);                    // cosh(sigma) e^-sigma
+    const double ssig = fma(S.s, Dl.c, S.c * Dl.s);                    // sinh(sigma) e^-sigma
+    const double Dh = fma((w * w) * (rr * rsn), R.s * S.s, -4.0 * sd2 * es2);
+    const double fh = (krho * c2) * rcp_fast(Dh);
+    Elem E;
+    E.k11 = (fh * rsn) * fma(w * R.s, S.c, -sdcd2 * es2);
+    E.k12 = fma(fh, fma(2.0 * sd2, es2, w * (R.s * S.s)), -mu * (2.0 - b));
+    E.k13 = (fh * rsn) * (S.e * fma(2.0 * csig, Dl.s, -w * R.s));
+    E.k14 = -2.0 * fh * ssig * Dl.s * S.e;
+    E.k22 = (fh * rr) * fma(sdcd2, es2, w * (R.c * S.s));
+    E.k24 = -(fh * rr) * fma(2.0 * csig * Dl.s, S.e, w * S.s * R.e);
+    return E;
+}
+
+// P wave hyperbolic, S wave trigonometric (beta_e < c < alpha_e): the direct formulas with
+// the P-wave terms scaled by e^-th_r (overflow-free for th_r up to 700).
+__device__ __forceinline__ Elem elem_stable_ht(double kh, double c2, double ia2, double ib2,
+                                               double krho, double mu, unsigned tab)
+{
+    double r, rr;
+    sqrt_rsqrt(fma(-c2, ia2, 1.0), r, rr);
+    const double qb = fma(-c2, ib2, 1.0);
+    const ExpScaled R = exp_scaled(kh * r, tab);
+    const double Cr = R.c, XSr = r * R.s, SXr = R.s * rr, er = R.e;
+    double Cs, XSs, SXs;
+    wave_trig(qb, kh, Cs, XSs, SXs);
+    const double Dh = fma(SXr, SXs, fma(XSr, XSs, 2.0 * fma(-Cr, Cs, er)));
+    const double fh = (krho * c2) * rcp_fast(Dh);
+    Elem E;
+    E.k11 = fh * fma(Cr, SXs, -XSr * Cs);
+    E.k12 = fma(fh, fma(-XSr, XSs, fma(Cr, Cs, -er)), -mu * (1.0 + qb));
+    E.k13 = fh * fma(-er, SXs, XSr);
+    E.k14 = fh * fma(er, Cs, -Cr);
+    E.k22 = fh * fma(SXr, Cs, -Cr * XSs);
+    E.k24 = fh * fma(er, XSs, -SXr);
+    return E;
+}
+
+__device__ __forceinline__ Elem layer_elem_stable(const LayerConst &L, double c2, unsigned tab)
+{
+    const double qa = fma(-c2, L.ia2, 1.0), qb = fma(-c2, L.ib2, 1.0);
+    if (qa > 0.0 && qb > 0.0) return elem_stable_hh(L.kh, c2, L.ia2, L.ib2, L.krho, L.mu, tab);
+    if (qa > 0.0) return elem_stable_ht(L.kh, c2, L.ia2, L.ib2, L.krho, L.mu, tab);
+    double t[6];   // both trigonometric: bounded functions, the direct formulas
+    waves_general(qa, qb, L.kh, t, tab);
+    return elem_from_triples(t[0], t[1], t[2], t[3], t[4], t[5], L.krho, L.mu, c2);
+}
+
 // -------------------------------------------------------------- wavelength-free terms
 // The square roots r_e = sqrt(1 - c^2/alpha_e^2), s_e = sqrt(1 - c^2/beta_e^2) and the
 // half-space's k-free factors depend on the model and c but NOT on the wavelength, so the
@@ -509,7 +617,10 @@ __device__ __forceinline__ HsRoot halfspace_root(double ia2, double ib2, double 
     if (qb > 0.0) {
         R.r = qa * rsqrt_fast(qa);
         R.s = qb * rsqrt_fast(qb);
-        R.gw = w * rcp_fast(1.0 - R.r * R.s);
+        // 1 - rs = (a + b - ab)/(1 + rs), a = c^2/alpha^2, b = c^2/beta^2 = w: no cancellation
+        // as c -> 0 (the direct 1 - rs loses ~log10(1/(1-rs)) digits there)
+        const double a = c2 * ia2;
+        R.gw = (w * (1.0 + R.r * R.s)) * rcp_fast(fma(-a, w, a + w));
         R.t = 0.0;
         R.kase = 0;
     } else if (qa > 0.0) {
@@ -853,7 +964,7 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
 // `vel` (shared memory).  `maybe_near` = false means c is already the S4-perturbed velocity
 // (the scan resolves S4 per warp for its 32 velocities, see scan_kernel), which skips the
 // per-lane S4 loop.
-template <bool WANT_VALUE, int NFIX = 0>
+template <bool WANT_VALUE, int NFIX = 0, bool STABLE = false>
 __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
                                         const double *__restrict__ vel,
                                         unsigned tab, int Nrt, double c,
@@ -863,7 +974,11 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
     const double cp = maybe_near ? perturb_velocity(vel, 2 * (N + 1), c) : c;
     const double c2 = cp * cp;
     return det_core<WANT_VALUE, NFIX, MASW_LAYER_UNROLL>(
-        N, [&](int e) { return layer_elem(load_lc(lc + e), c2, tab); },
+        N,
+        [&](int e) {
+            if constexpr (STABLE) return layer_elem_stable(load_lc(lc + e), c2, tab);
+            else return layer_elem(load_lc(lc + e), c2, tab);
+        },
         [&] {
             const LayerConst H = load_lc(lc + N);
             return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.mu);

@@ -45,7 +45,11 @@ struct ScanArgs {
     unsigned grid_mask;  // Workspace::grid_err bits that invalidate the call (0x1F, 0x7F with C_e)
     int sched;           // 0 work-stealing queue, 1 static contiguous, 2 static modular
     unsigned long long *team_dets;  // per-team algorithmic det counts (nullable)
+    int stable;          // MASW_STABLE: the scaled, cancellation-free element (row kernel)
 };
+
+// grid_mask bit: the call uses the stable element, range guard k h <= 700 instead of 350
+constexpr unsigned kGridStable = 0x100u;
 
 // Launchers (masw_kernels.cu).  Each returns the cudaError_t of its launch.
 cudaError_t launch_validate(const ModelArgs &m, const double *lam, int64_t L, const double *c,
@@ -62,7 +66,7 @@ cudaError_t launch_argmin(const double *misfit, int64_t M, int64_t *best, double
                           cudaStream_t st);
 cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, const double *c,
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
-                            cudaStream_t st);
+                            cudaStream_t st, bool stable = false);
 int auto_team_warps(int64_t rows, int64_t V, int device);
 // Model-major scan (ensembles): suitable when there are many (model, wavelength-block) items
 // and the per-warp caches fit two CTAs per SM; same outputs as launch_scan.

@@ -41,14 +41,15 @@ long long launches() { return g_launches.load(std::memory_order_relaxed); }
 
 // ------------------------------------------------------------------ validation
 
-__device__ __forceinline__ bool ws_range_bad(const Workspace *ws)
+__device__ __forceinline__ bool ws_range_bad(const Workspace *ws, bool stable)
 {
     // max_i,e fl(fl(2pi/lambda_i) * h_e) = fl(fl(2pi/lambda_min) * h_max): both roundings are
-    // monotone, so this is exactly the per-pair guard of include/masw.h.
+    // monotone, so this is exactly the per-pair guard of include/masw.h (350, or 700 for the
+    // scaled elements of MASW_STABLE).
     const double lam_min = __longlong_as_double((long long)~ws->lam_min_nbits);
     const double h_max = __longlong_as_double((long long)ws->h_max_bits);
     const double kmax = kTwoPi / lam_min;
-    return kmax * h_max > kMaxKH;
+    return kmax * h_max > (stable ? kMaxKHStable : kMaxKH);
 }
 
 // max over the call's rows and layers of k h_e (validated: <= 350) -> cosh/sinh table rows.
@@ -66,7 +67,7 @@ __device__ __forceinline__ bool ws_invalid(const Workspace *ws, unsigned grid_ma
     if (ws->grid_err & grid_mask) return true;
     if (check_models) {
         if (ws->model_err != 0ull) return true;
-        if (ws_range_bad(ws)) return true;
+        if (ws_range_bad(ws, (grid_mask & kGridStable) != 0)) return true;
     }
     return false;
 }
@@ -200,7 +201,7 @@ constexpr int scan_min_blocks()
     return BLOCK == 256 ? MASW_SCAN_MINB : 1;
 }
 
-template <int TEAM, int BLOCK, int NFIX>
+template <int TEAM, int BLOCK, bool STABLE>
 __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(ScanArgs a)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             int s = 0;
             bool bad = false;
             if (j < V) {
-                const DetOut d = det_K<false, NFIX>(lc, vel, ta, N, c, false);
+                const DetOut d = det_K<false, 0, STABLE>(lc, vel, ta, N, c, false);
                 s = d.sign;
                 bad = d.bad;
                 ++my_eval;
@@ -668,16 +669,16 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
     return team;
 }
 
-template <int TEAM, int BLOCK, int NFIX>
+template <int TEAM, int BLOCK, bool STABLE>
 static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
                                  long long *teams_out, bool dry = false)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     const size_t smem = kExpTabBytes + round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
                         (size_t)TEAMS * team_model_bytes(a.mod.N);
-    auto kern = scan_kernel<TEAM, BLOCK, NFIX>;
+    auto kern = scan_kernel<TEAM, BLOCK, STABLE>;
     const int sms = sm_count(device);
-    const long long key = ((long long)device << 48) | ((long long)NFIX << 40) |
+    const long long key = ((long long)device << 48) | ((long long)STABLE << 40) |
                           ((long long)TEAM << 32) | (long long)smem;
     int per_sm = 0;
     {
@@ -686,7 +687,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
         if (it != g_occ_cache.end()) per_sm = it->second;
     }
     {
-        cudaError_t e = ensure_smem_optin(kern, device, 16 + TEAM);
+        cudaError_t e = ensure_smem_optin(kern, device, 16 + TEAM + (STABLE ? 32 : 0));
         if (e != cudaSuccess) return e;
     }
     if (per_sm == 0) {
@@ -716,12 +717,22 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
 static cudaError_t dispatch_scan(const ScanArgs &a, int team_warps, cudaStream_t st, int device,
                                  long long *teams_out, bool dry)
 {
+    if (a.stable) {
+        switch (team_warps) {
+            case 1: return launch_scan_t<1, 256, true>(a, st, device, teams_out, dry);
+            case 2: return launch_scan_t<2, 256, true>(a, st, device, teams_out, dry);
+            case 4: return launch_scan_t<4, 256, true>(a, st, device, teams_out, dry);
+            case 8: return launch_scan_t<8, 256, true>(a, st, device, teams_out, dry);
+            case 16: return launch_scan_t<16, 512, true>(a, st, device, teams_out, dry);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (team_warps) {
-        case 1: return launch_scan_t<1, 256, 0>(a, st, device, teams_out, dry);
-        case 2: return launch_scan_t<2, 256, 0>(a, st, device, teams_out, dry);
-        case 4: return launch_scan_t<4, 256, 0>(a, st, device, teams_out, dry);
-        case 8: return launch_scan_t<8, 256, 0>(a, st, device, teams_out, dry);
-        case 16: return launch_scan_t<16, 512, 0>(a, st, device, teams_out, dry);
+        case 1: return launch_scan_t<1, 256, false>(a, st, device, teams_out, dry);
+        case 2: return launch_scan_t<2, 256, false>(a, st, device, teams_out, dry);
+        case 4: return launch_scan_t<4, 256, false>(a, st, device, teams_out, dry);
+        case 8: return launch_scan_t<8, 256, false>(a, st, device, teams_out, dry);
+        case 16: return launch_scan_t<16, 512, false>(a, st, device, teams_out, dry);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -920,13 +931,14 @@ cudaError_t launch_argmin(const double *misfit, int64_t M, int64_t *best, double
 
 // ------------------------------------------------------------------ det grid (debug)
 
+template <bool STABLE>
 __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const double *lam,
                                                        int64_t L, const double *c, int64_t V,
                                                        double *mre, double *mim, int32_t *ex,
                                                        const Workspace *ws)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    if (ws_invalid(ws, 0x1Fu, true)) return;
+    if (ws_invalid(ws, 0x1Fu | (STABLE ? kGridStable : 0u), true)) return;
     unsigned char *tab = smem;
     exp_scale_fill(tab, ws_exp_rows(ws));
     const int N = mod.N;
@@ -950,7 +962,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
     __syncthreads();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
-    const DetOut d = det_K<true>(lc, vel, smem_addr(tab), N, c[j]);
+    const DetOut d = det_K<true, 0, STABLE>(lc, vel, smem_addr(tab), N, c[j]);
     const int64_t o = i * V + j;
     mre[o] = d.mre;
     mim[o] = d.mim;
@@ -959,15 +971,16 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
 
 cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, const double *c,
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
-                            cudaStream_t st)
+                            cudaStream_t st, bool stable)
 {
     const size_t smem = kExpTabBytes + team_model_bytes(m.N);
     int dev = 0;
     cudaGetDevice(&dev);   // the C-ABI's DeviceScope has made the call's device current
-    cudaError_t e = ensure_smem_optin(det_grid_kernel, dev, 2);
+    auto kern = stable ? det_grid_kernel<true> : det_grid_kernel<false>;
+    cudaError_t e = ensure_smem_optin(kern, dev, stable ? 3 : 2);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((V + 255) / 256), (unsigned)L);
-    det_grid_kernel<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws);
+    kern<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws);
     count_launch();
     return cudaGetLastError();
 }

@@ -24,6 +24,7 @@ IDX_NO_CHANGE, IDX_NONFINITE = -1, -2
 ASYNC, TIME_SCAN = 0x1, 0x2
 SCHED_CONTIGUOUS, SCHED_MODULAR, TEAM_STATS = 0x4, 0x8, 0x10
 SCHED_ROWS, SCHED_MODELS = 0x20, 0x40   # force the row / model-major scan kernel
+STABLE = 0x80   # cancellation-free, exponentially scaled element (f3), k h <= 700
 MAX_LAYERS = 64
 
 
@@ -247,8 +248,9 @@ def masw_argmin(misfit, *, stream=None, flags=0):
     return bb.obj, bv.obj
 
 
-def masw_det_grid(h, alpha, beta, rho, lam, c, *, stream=None):
-    """Full (λ, c) determinant grid (debug/parity) → (mant complex [L][V], exp2 [L][V])."""
+def masw_det_grid(h, alpha, beta, rho, lam, c, *, flags=0, stream=None):
+    """Full (λ, c) determinant grid (debug/parity) → (mant re [L][V], mant im, exp2 [L][V]).
+    flags=STABLE evaluates the cancellation-free, exponentially scaled element (f3)."""
     bh, ba, bb, br = (_Buf(x, np.float64) for x in (h, alpha, beta, rho))
     bl, bc = _Buf(lam, np.float64), _Buf(c, np.float64)
     L, V = len(bl.obj), len(bc.obj)
@@ -256,7 +258,7 @@ def masw_det_grid(h, alpha, beta, rho, lam, c, *, stream=None):
     im = _Buf(_empty_like_kind(bl, (L, V), np.float64), np.float64)
     ex2 = _Buf(_empty_like_kind(bl, (L, V), np.int32), np.int32)
     mod = _Model(len(bh.obj), bh.ptr, ba.ptr, bb.ptr, br.ptr)
-    ex = _exec(bl, 0, 0, stream)
+    ex = _exec(bl, 0, flags, stream)
     _check(lib().masw_det_grid(ctypes.byref(mod), bl.ptr, L, bc.ptr, V, re.ptr, im.ptr,
                                ex2.ptr, ctypes.byref(ex)), "masw_det_grid")
     return re.obj, im.obj, ex2.obj

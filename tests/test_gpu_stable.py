@@ -1,0 +1,141 @@
+"""the stable element (MASW_STABLE) against 50-digit mpmath.
+
+The direct App. A formulas lose accuracy as c -> 0 (reading S15: the entries are O(c^4) /
+O(c^2) differences of O(cosh^2) terms) and overflow for k h > ~350 (reading S9).  The
+stable element rewrites every bracket in cancellation-free form and scales the hyperbolic
+functions by e^-th.  The reference is mpmath at 50 digits
+evaluating App. A on the same fp64 inputs (fp64 wavenumber fl(2 pi / lambda)), so only the
+arithmetic differs -- the naive fp64 oracle is not accurate enough to judge this path.
+"""
+import numpy as np
+import pytest
+
+import synth
+from test_oracle_pins import _mp_det
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def masw():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2003_02256_b200 as m
+
+    m.lib()
+    return m
+
+
+def _grid_det(masw, a, lam, c, flags):
+    re, im, ex = masw.masw_det_grid(*a, np.array([lam]), np.asarray(c, dtype=np.float64),
+                                    flags=flags)
+    return (re[0] + 1j * im[0]) * np.ldexp(1.0, ex[0])
+
+
+def _rel_errors(masw, a, lam, cs, flags):
+    import mpmath as mp
+
+    got = _grid_det(masw, a, lam, cs, flags)
+    out = []
+    for g, c in zip(got, cs):
+        want = _mp_det(*a, lam, float(c), k_double=True)
+        g = mp.mpc(float(np.real(g)), float(np.imag(g)))
+        out.append(float(abs(g - want) / abs(want)))
+    return np.array(out)
+
+
+FRACS = np.array([0.02, 0.05, 0.1, 0.2, 0.3, 0.5, 0.8])
+
+
+@pytest.mark.parametrize("lam", [0.5, 5.0, 40.0, 100.0])
+def test_stable_element_small_c_vs_mpmath(masw, lam):
+    """c = 0.02 .. 0.8 beta_min on the C2 model: the stable element stays within 1e-11 of
+    50-digit arithmetic where the direct formulas lose up to ~1e-3 (reading S15)."""
+    m = synth.maswaves_model()
+    a = (m.h[0], m.alpha[0], m.beta[0], m.rho[0])
+    cs = FRACS * float(m.beta[0].min()) * (1.0 + 1e-7)     # off the S4 tolerance band
+    err_s = _rel_errors(masw, a, lam, cs, masw.STABLE)
+    assert err_s.max() < 1e-11, (lam, err_s)
+
+
+def test_stable_element_fixes_what_the_direct_formulas_lose(masw):
+    """The comparison is meaningful: at long wavelength and small c the default (direct)
+    element is far from 50-digit arithmetic, the stable one is not."""
+    m = synth.maswaves_model()
+    a = (m.h[0], m.alpha[0], m.beta[0], m.rho[0])
+    cs = np.array([0.02, 0.05, 0.1]) * float(m.beta[0].min()) * (1.0 + 1e-7)
+    err_d = _rel_errors(masw, a, 100.0, cs, 0)
+    err_s = _rel_errors(masw, a, 100.0, cs, masw.STABLE)
+    assert err_d.max() > 1e-6 and err_s.max() < 1e-11, (err_d, err_s)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_stable_element_random_models_vs_mpmath(masw, seed):
+    """Random C5 models, random wavelengths, c from 0.02 beta_min to above alpha-ish values
+    (all three wave cases) -- within 1e-10 of 50-digit arithmetic wherever the determinant is
+    not at a root (|det| >= 1e-6 of its neighbours' scale)."""
+    rng = np.random.default_rng(seed)
+    w = synth.workload("ensemble", M=50)
+    worst = 0.0
+    for _ in range(6):
+        mi = int(rng.integers(50))
+        a = (w.models.h[mi], w.models.alpha[mi], w.models.beta[mi], w.models.rho[mi])
+        lam = float(rng.choice(w.lam))
+        bmin = float(a[2].min())
+        cs = np.sort(np.r_[rng.uniform(0.02, 0.95, 4) * bmin, rng.uniform(1.05, 2.5, 2) * bmin])
+        err = _rel_errors(masw, a, lam, cs, masw.STABLE)
+        worst = max(worst, float(err.max()))
+    assert worst < 1e-10, worst
+
+
+def test_stable_element_thick_layers_beyond_the_direct_range(masw):
+    """k h up to 700 (a 50 m layer at lambda = 0.5 m: k h = 628): the direct element is
+    rejected (MASW_E_RANGE, cosh would overflow), the scaled one matches 50-digit arithmetic;
+    beyond 700 both are rejected."""
+    h = np.array([2.0, 50.0])
+    beta = np.array([150.0, 220.0, 400.0])
+    alpha = np.full(3, 1440.0)
+    rho = np.array([1800.0, 1900.0, 2000.0])
+    a = (h, alpha, beta, rho)
+    cs = np.array([60.0, 120.0, 170.0, 260.0, 500.0])
+    with pytest.raises(masw.MaswError) as e:
+        masw.masw_det_grid(*a, np.array([0.5]), cs)
+    assert e.value.code == masw.E_RANGE
+    err = _rel_errors(masw, a, 0.5, cs, masw.STABLE)
+    assert err.max() < 1e-10, err
+    with pytest.raises(masw.MaswError) as e:
+        masw.masw_det_grid(np.array([2.0, 60.0]), alpha, beta, rho, np.array([0.5]), cs,
+                           flags=masw.STABLE)
+    assert e.value.code == masw.E_RANGE
+
+
+@pytest.mark.parametrize("name", ["tiny", "maswaves"])
+def test_stable_scan_same_curves(masw, orc, name):
+    """The scan with the stable element gives C_t within the parity rule of the oracle (the
+    sign changes sit at c ~ 0.9 beta, where both elements are accurate)."""
+    import masw_parity as parity
+
+    w = synth.workload(name)
+    a = (w.models.h[0], w.models.alpha[0], w.models.beta[0], w.models.rho[0])
+    st, ct, idx = masw.masw_curve(*a, w.lam, w.c, flags=masw.STABLE)
+    ost, oct_, oidx, ond = orc.curve(*a, w.lam, w.c)
+    assert st == ost
+    ok, exact, one = parity.ct_acceptable(orc, a, w.lam, w.c, idx, oidx)
+    assert ok.all()
+
+
+def test_stable_ensemble_matches_default_and_oracle(masw, orc):
+    import masw_parity as parity
+
+    w = synth.workload("ensemble", M=60)
+    mods = w.models
+    r = masw.masw_curves_ensemble(mods.h, mods.alpha, mods.beta, mods.rho, w.lam, w.c, w.ce,
+                                  flags=masw.STABLE)
+    o = orc.ensemble(mods, w.lam, w.c, w.ce)
+    assert r.status == o["status"]
+    for m in range(mods.n_models):
+        a = (mods.h[m], mods.alpha[m], mods.beta[m], mods.rho[m])
+        ok, exact, one = parity.ct_acceptable(orc, a, w.lam, w.c, r.idx[m], o["idx"][m])
+        assert ok.all()
