@@ -427,28 +427,31 @@ def other_configs(masw, torch, dev):
     """Single-curve configs C1-C4 on one GPU (device pointers): latency / throughput."""
     out = {}
     t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
-    for name, kw, reps in [("tiny", {}, 50), ("maswaves", {}, 50),
-                           ("uniform", {"tier": 200.0}, 5), ("realistic", {}, 5)]:
+    # "realistic_stable": C4 through the stable element (SURVEY.md §8(f) f3, MASW_STABLE)
+    for key, name, kw, reps, fl in [("tiny", "tiny", {}, 50, 0), ("maswaves", "maswaves", {}, 50, 0),
+                                    ("uniform", "uniform", {"tier": 200.0}, 5, 0),
+                                    ("realistic", "realistic", {}, 5, 0),
+                                    ("realistic_stable", "realistic", {}, 5, masw.STABLE)]:
         w = synth.workload(name, **kw)
         m = w.models
         args = [t(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)]
         lam, c = t(w.lam), t(w.c)
         for _ in range(3):
-            masw.masw_curve(*args, lam, c)
+            masw.masw_curve(*args, lam, c, flags=fl)
         torch.cuda.synchronize()
         ts, scans = [], []
         for _ in range(reps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            masw.masw_curve(*args, lam, c, flags=masw.TIME_SCAN)
+            masw.masw_curve(*args, lam, c, flags=masw.TIME_SCAN | fl)
             e1.record()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
             scans.append(masw.masw_last_scan_ms())
         alg, ev = masw.masw_last_work()
         med = statistics.median(ts)
-        out[name] = {"call_ms_median": med, "scan_ms_median": statistics.median(scans),
+        out[key] = {"call_ms_median": med, "scan_ms_median": statistics.median(scans),
                      "dets": alg, "dets_per_s": alg / (med / 1e3),
                      "curves_per_s": 1e3 / med, "note": w.note}
     return out

@@ -52,7 +52,7 @@ def main():
                                                        flags=masw.TIME_SCAN | xflags)
             else:
                 fn = lambda: masw.masw_curve(*[a[0] for a in args], lam, c, team_warps=team,
-                                             flags=masw.TIME_SCAN)
+                                             flags=masw.TIME_SCAN | xflags)
             t = time_call(fn)
             alg, ev = masw.masw_last_work()
             kms = masw.masw_last_scan_ms()
