@@ -149,8 +149,12 @@ __device__ __forceinline__ double lds_f64(unsigned a)
 __device__ __forceinline__ int lds_s32(unsigned a)
 {
     int v;
-    asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
+}
+__device__ __forceinline__ void sts_s32(unsigned a, int v)
+{
+    asm volatile("st.shared.s32 [%0], %1;" : : "r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ LayerConst load_lc_at(unsigned a)
 {

@@ -417,6 +417,7 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
     return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
                    2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
                    (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
+                   (unsigned)kModelRows * 4u +                             // carried sign per row
                    32u * lane_cache_stride(N));                            // per-lane roots
 }
 
@@ -432,8 +433,9 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
     double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
     double *kr = vel + 2 * (N + 1);
+    int *carry = reinterpret_cast<int *>(kr + kModelRows);              // per row: last sign
     const unsigned stride = lane_cache_stride(N);
-    unsigned char *cl = reinterpret_cast<unsigned char *>(kr + kModelRows) + (unsigned)lane * stride;
+    unsigned char *cl = reinterpret_cast<unsigned char *>(carry + kModelRows) + (unsigned)lane * stride;
 
     Workspace *ws = a.ws;
     if (threadIdx.x == 0) {
@@ -447,7 +449,8 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
 
-    const int64_t M = a.mod.M, L = a.L, V = a.V;
+    const int64_t M = a.mod.M, L = a.L;
+    const int V = (int)a.V;                 // < 2^31 (idx is int32; checked by the C ABI)
     const int64_t groups = (L + kModelRows - 1) / kModelRows;
     const int64_t items = M * groups;
     const double *__restrict__ cg = a.c;
@@ -480,15 +483,22 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             vel[2 * e] = al;
             vel[2 * e + 1] = be;
         }
-        for (int r = lane; r < nr; r += 32) kr[r] = kTwoPi / a.lam[i0 + r];   // reading S2
+        for (int r = lane; r < nr; r += 32) {
+            kr[r] = kTwoPi / a.lam[i0 + r];   // reading S2
+            carry[r] = 0;
+        }
         __syncwarp();
         const unsigned ma = opaque(smem_addr(mc));
         const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
+        const unsigned ka = opaque(smem_addr(kr));
+        const unsigned ya = opaque(smem_addr(carry));
 
-        const unsigned long long all = (nr == 64) ? ~0ull : ((1ull << nr) - 1ull);
-        unsigned long long done = 0, cpos = 0, cneg = 0;   // per row: found, carry sign
-        for (int64_t base = 0; base < V && done != all; base += 32) {
-            const int64_t j = base + lane;
+        // rows of the item in two 32-bit halves: pending = not yet found
+        unsigned pend0 = (nr >= 32) ? ~0u : ((1u << nr) - 1u);
+        unsigned pend1 = (nr > 32) ? ((nr == 64) ? ~0u : ((1u << (nr - 32)) - 1u)) : 0u;
+        unsigned ev32 = 0;
+        for (int base = 0; base < V && (pend0 | pend1); base += 32) {
+            const int j = base + lane;
             const bool valid = j < V;
             double c = cg[valid ? j : V - 1];
             {   // reading S4, as in scan_kernel
@@ -523,71 +533,79 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             }
             const unsigned ca = opaque(smem_addr(cl));
             const unsigned hca = ca + 32u * (unsigned)N;
-            for (unsigned long long pend = all & ~done; pend; pend &= pend - 1) {
-                const int r = __ffsll((long long)pend) - 1;
-                const double k = kr[r];
-                int s = 0;
-                bool bad = false;
-                if (valid) {
-                    const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
-                        N,
-                        [&](int e) {
-                            const unsigned o = 32u * (unsigned)e;
-                            return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
-                                                   lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
-                        },
-                        [&] {
-                            const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
-                            const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
-                            HsRoot h;
-                            h.r = rs.x;
-                            h.s = rs.y;
-                            h.gw = gt.x;
-                            h.t = gt.y;
-                            h.kase = lds_s32(hca + 32u);
-                            return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
-                        });
-                    s = d.sign;
-                    bad = d.bad;
-                    ++my_eval;
-                }
-                int sprev = __shfl_up_sync(FULL, s, 1);
-                if (lane == 0) sprev = ((cpos >> r) & 1ull) ? 1 : (((cneg >> r) & 1ull) ? -1 : 0);
-                const bool ev = valid && (bad || (j > 0 && s != sprev));
-                const unsigned mask = __ballot_sync(FULL, ev);
-                if (mask) {
-                    const int64_t first = base + (__ffs(mask) - 1);
-                    if (j == first) {
-                        const int64_t o = m * L + i0 + r;
-                        if (bad) {
-                            a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
-                            if (a.idx) a.idx[o] = -2;
-                            my_status |= 2u;
-                        } else {
-                            a.ct[o] = cg[j];
-                            if (a.idx) a.idx[o] = (int32_t)j;
-                        }
-                        my_alg += (unsigned long long)(j + 1);
+#pragma unroll 1
+            for (int half = 0; half < 2; ++half) {
+                unsigned pend = half ? pend1 : pend0;
+                unsigned found = 0;
+                while (pend) {
+                    const int r = half * 32 + __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    const double k = lds_f64(ka + 8u * (unsigned)r);
+                    int s = 0;
+                    bool bad = false;
+                    if (valid) {
+                        const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
+                            N,
+                            [&](int e) {
+                                const unsigned o = 32u * (unsigned)e;
+                                return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
+                                                       lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
+                            },
+                            [&] {
+                                const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
+                                const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
+                                HsRoot h;
+                                h.r = rs.x;
+                                h.s = rs.y;
+                                h.gw = gt.x;
+                                h.t = gt.y;
+                                h.kase = lds_s32(hca + 32u);
+                                return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
+                            });
+                        s = d.sign;
+                        bad = d.bad;
+                        ++ev32;
                     }
-                    team_alg += (unsigned long long)(first + 1);
-                    done |= 1ull << r;
-                } else {
-                    const int last = __shfl_sync(FULL, s, 31);
-                    cpos = (cpos & ~(1ull << r)) | ((unsigned long long)(last > 0) << r);
-                    cneg = (cneg & ~(1ull << r)) | ((unsigned long long)(last < 0) << r);
+                    int sprev = __shfl_up_sync(FULL, s, 1);
+                    if (lane == 0) sprev = lds_s32(ya + 4u * (unsigned)r);
+                    const bool ev = valid && (bad || (j > 0 && s != sprev));
+                    const unsigned mask = __ballot_sync(FULL, ev);
+                    if (mask) {
+                        const int first = base + (__ffs(mask) - 1);
+                        if (j == first) {
+                            const int64_t o = m * L + i0 + r;
+                            if (bad) {
+                                a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+                                if (a.idx) a.idx[o] = -2;
+                                my_status |= 2u;
+                            } else {
+                                a.ct[o] = cg[j];
+                                if (a.idx) a.idx[o] = (int32_t)j;
+                            }
+                            my_alg += (unsigned long long)(j + 1);
+                        }
+                        team_alg += (unsigned long long)(first + 1);
+                        found |= 1u << (r - half * 32);
+                    } else if (lane == 31) {
+                        sts_s32(ya + 4u * (unsigned)r, s);   // carried to the next chunk
+                    }
                 }
+                if (half) pend1 &= ~found; else pend0 &= ~found;
             }
-            __syncwarp();   // the next chunk rewrites this lane's roots
+            __syncwarp();   // the next chunk rewrites this lane's roots; carries are visible
         }
-        for (unsigned long long pend = all & ~done; pend; pend &= pend - 1) {
-            const int r = __ffsll((long long)pend) - 1;
-            team_alg += (unsigned long long)V;
-            if (lane == 0) {
-                const int64_t o = m * L + i0 + r;
-                a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
-                if (a.idx) a.idx[o] = -1;
-                my_status |= 1u;
-                my_alg += (unsigned long long)V;
+        my_eval += ev32;
+        for (int half = 0; half < 2; ++half) {
+            for (unsigned pend = half ? pend1 : pend0; pend; pend &= pend - 1) {
+                const int r = half * 32 + __ffs(pend) - 1;
+                team_alg += (unsigned long long)V;
+                if (lane == 0) {
+                    const int64_t o = m * L + i0 + r;
+                    a.ct[o] = __longlong_as_double(0x7ff8000000000000ll);
+                    if (a.idx) a.idx[o] = -1;
+                    my_status |= 1u;
+                    my_alg += (unsigned long long)V;
+                }
             }
         }
         __syncwarp();   // the next item rewrites this warp's constants
