@@ -842,33 +842,35 @@ __device__ __forceinline__ StepOut gepp_step(double (&R)[4][NC], double (&Ri)[4]
 // NFIX > 0 compiles the determinant for exactly NFIX layers (fully unrolled); NFIX = 0 takes
 // N at run time, its node loop unrolled UNROLL times (measured on B200: 2 is 1.7 % faster
 // for the model-major kernel at N = 6, 1 is 4 % faster for the row kernel at N = 10).
-template <bool WANT_VALUE, int NFIX, int UNROLL, class ElemFn, class HsFn>
-__device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
-{
-    const int N = NFIX > 0 ? NFIX : Nrt;
+// State of one streamed banded-GEPP determinant: the previous layer's element P, the two
+// rows X left over by the last step, and the sign / zero / non-finite bookkeeping.
+//
+// Sign, zero and non-finite bookkeeping in integer ops on the pivots' high words (off the FP64
+// pipe): sgn accumulates the XOR of the pivots' sign bits; a zero pivot has key 0, an Inf/NaN
+// pivot a key >= 0x7ff00000 (NaN keys exceed every finite key, so a NaN entry is always picked
+// as a pivot or reaches the last 2x2 through the updates).
+template <bool WANT_VALUE>
+struct DetState {
+    Elem P;
+    double X[2][4];
+    int perm;
+    unsigned sgn, kmin, kmax;
+    DetAcc acc;
 
-    // Sign, zero and non-finite bookkeeping in integer ops on the pivots' high words (off the
-    // FP64 pipe): sgn accumulates the XOR of the pivots' sign bits; a zero pivot has key 0, an
-    // Inf/NaN pivot a key >= 0x7ff00000 (NaN keys exceed every finite key, so a NaN entry is
-    // always picked as a pivot or reaches the last 2x2 through the updates).
-    int perm = 0;
-    unsigned sgn = 0;
-    unsigned kmin = 0x7fffffffu, kmax = 0u;
-    DetAcc acc{1.0, 0};
+    __device__ __forceinline__ void init(const Elem &E)
+    {
+        P = E;
+        X[0][0] = E.k11; X[0][1] = E.k12; X[0][2] = E.k13; X[0][3] = E.k14;
+        X[1][0] = E.k12; X[1][1] = E.k22; X[1][2] = -E.k14; X[1][3] = E.k24;
+        perm = 0;
+        sgn = 0u;
+        kmin = 0x7fffffffu;
+        kmax = 0u;
+        acc = DetAcc{1.0, 0};
+    }
 
-    Elem P = elem(0);
-    double X[2][4] = {{P.k11, P.k12, P.k13, P.k14}, {P.k12, P.k22, -P.k14, P.k24}};
-
-    auto node_step = [&](int t) {
-        const Elem Q = elem(t + 1);
-        double R[4][6] = {
-            {X[0][0], X[0][1], X[0][2], X[0][3], 0.0, 0.0},
-            {X[1][0], X[1][1], X[1][2], X[1][3], 0.0, 0.0},
-            {P.k13, -P.k14, P.k11 + Q.k11, Q.k12 - P.k12, Q.k13, Q.k14},
-            {P.k14, P.k24, Q.k12 - P.k12, P.k22 + Q.k22, -Q.k14, Q.k24}};
-        double Ri[4][6];   // unused (real step): NR = 0
-        double Xi[2][4];
-        const StepOut so = gepp_step<6, 0>(R, Ri, X, Xi);
+    __device__ __forceinline__ void book(const StepOut &so)
+    {
         sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
         kmin = min(kmin, min((unsigned)so.key0, (unsigned)so.key1));
         kmax = max(kmax, max((unsigned)so.key0, (unsigned)so.key1));
@@ -877,91 +879,121 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
             acc.mul(so.piv0);
             acc.mul(so.piv1);
         }
+    }
+
+    // one node step with the next layer's element Q
+    __device__ __forceinline__ void step(const Elem &Q)
+    {
+        double R[4][6] = {
+            {X[0][0], X[0][1], X[0][2], X[0][3], 0.0, 0.0},
+            {X[1][0], X[1][1], X[1][2], X[1][3], 0.0, 0.0},
+            {P.k13, -P.k14, P.k11 + Q.k11, Q.k12 - P.k12, Q.k13, Q.k14},
+            {P.k14, P.k24, Q.k12 - P.k12, P.k22 + Q.k22, -Q.k14, Q.k24}};
+        double Ri[4][6];   // unused (real step): NR = 0
+        double Xi[2][4];
+        book(gepp_step<6, 0>(R, Ri, X, Xi));
         P = Q;
-    };
+    }
+
+    // last step with the half-space element: node N-1 columns real, node N columns complex
+    // (NR = 2) -- or real when c < beta_N (K_hs real, the common case)
+    __device__ __forceinline__ DetOut finish(const HalfSpace &H)
+    {
+        double dre, dim;
+        if (H.real) {
+            double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
+                              {X[1][0], X[1][1], X[1][2], X[1][3]},
+                              {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
+                              {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
+            double Ri[4][4];   // unused: NR = 0
+            double Y[2][2], Yi[2][2];
+            book(gepp_step<4, 0>(R, Ri, Y, Yi));
+            dre = fma(Y[0][0], Y[1][1], -Y[0][1] * Y[1][0]);
+            dim = 0.0;
+        } else {
+            double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
+                              {X[1][0], X[1][1], X[1][2], X[1][3]},
+                              {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
+                              {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
+            double Ri[4][4] = {{0.0, 0.0, 0.0, 0.0},
+                               {0.0, 0.0, 0.0, 0.0},
+                               {0.0, 0.0, H.h11i, H.h12i},
+                               {0.0, 0.0, H.h12i, H.h22i}};
+            double Y[2][2], Yi[2][2];
+            book(gepp_step<4, 2>(R, Ri, Y, Yi));
+            // det of the last complex 2x2
+            dre = fma(Y[0][0], Y[1][1], -Yi[0][0] * Yi[1][1]) -
+                  fma(Y[0][1], Y[1][0], -Yi[0][1] * Yi[1][0]);
+            dim = fma(Y[0][0], Yi[1][1], Yi[0][0] * Y[1][1]) -
+                  fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
+        }
+        kmax = max(kmax, max((unsigned)mag_key(dre), (unsigned)mag_key(dim)));
+        // A zero pivot (key 0: the pivot column is zero, det K = 0 exactly) makes every later
+        // pivot NaN through the unguarded reciprocal; it takes precedence, as in the oracle's
+        // elimination, which stops there with det = 0.  Inputs are finite and the range
+        // guard S9 keeps every entry finite, so no Inf/NaN can precede a zero pivot.
+        const bool zero = (kmin == 0u) || (dre == 0.0);
+        const bool bad = (kmax >= 0x7ff00000u) && (kmin != 0u);
+        const bool neg = (perm != 0) ^ ((sgn >> 31) != 0) ^ (dre < 0.0);
+
+        DetOut out;
+        out.bad = bad;
+        out.sign = zero ? 0 : (neg ? -1 : 1);
+        out.mre = 0.0;
+        out.mim = 0.0;
+        out.e2 = 0;
+        if (WANT_VALUE && kmin != 0u) {
+            // value = (-1)^permutation * (prod pivots) * (dre + i dim)
+            const double ps = perm ? -acc.m : acc.m;
+            double re = ps * dre, im = ps * dim;
+            const double t = fmax(fabs(re), fabs(im));
+            if (t == 0.0 || !isfinite(t)) {
+                out.mre = re;
+                out.mim = im;
+                out.e2 = (t == 0.0) ? 0 : acc.e;
+            } else {
+                int ex;
+                frexp(t, &ex);
+                out.mre = ldexp(re, -ex);
+                out.mim = ldexp(im, -ex);
+                out.e2 = acc.e + ex;
+            }
+        }
+        return out;
+    }
+};
+
+// Determinant core (sign, optionally value) of K for N layers.  elem(e) returns the element
+// of layer e (0 <= e < N), hs() the half-space element.
+//
+// Elimination (reading S10/S11): banded GEPP streamed node by node.  The nodes' rows hold
+//   node 0:     [ top_0 | B_0 ]
+//   node t:     [ B_{t-1}^T | bottom_{t-1} + top_t | B_t ]
+//   node N:     [ B_{N-1}^T | bottom_{N-1} + K_hs ]
+// with top = [[k11, k12], [k12, k22]], bottom = [[k11, -k12], [-k12, k22]],
+// B = [[k13, k14], [-k14, k24]].  Step t eliminates node t's two columns from the two rows
+// left over by step t-1 and the two rows of node t+1.  Every column of nodes < N is real
+// (reading S3/S5), so the pivots and all but the last node's columns are real fp64; only
+// node N's columns (K_hs) are complex.  det K = (-1)^parity * prod pivots * det(last 2x2).
+// Cost per node: one layer element + one 4-row GEPP step, O(N) in total.
+// NFIX > 0 compiles the determinant for exactly NFIX layers (fully unrolled); NFIX = 0 takes
+// N at run time, its node loop unrolled UNROLL times (measured on B200: 2 is 1.7 % faster
+// for the model-major kernel at N = 6, 1 is 4 % faster for the row kernel at N = 10).
+template <bool WANT_VALUE, int NFIX, int UNROLL, class ElemFn, class HsFn>
+__device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
+{
+    const int N = NFIX > 0 ? NFIX : Nrt;
+    DetState<WANT_VALUE> st;
+    st.init(elem(0));
     if constexpr (NFIX > 0) {
 #pragma unroll
-        for (int t = 0; t + 1 < NFIX; ++t) node_step(t);
+        for (int t = 0; t + 1 < NFIX; ++t) st.step(elem(t + 1));
     } else {
         constexpr int kLayerUnroll = UNROLL;
 #pragma unroll kLayerUnroll
-        for (int t = 0; t + 1 < N; ++t) node_step(t);
+        for (int t = 0; t + 1 < N; ++t) st.step(elem(t + 1));
     }
-
-    const HalfSpace H = hs();
-
-    // Last step: node N-1 columns real, node N columns complex (NR = 2) -- or real when
-    // c < beta_N (K_hs real, the common case below the half-space shear velocity).
-    double dre, dim;
-    StepOut so;
-    if (H.real) {
-        double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
-                          {X[1][0], X[1][1], X[1][2], X[1][3]},
-                          {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
-                          {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
-        double Ri[4][4];   // unused: NR = 0
-        double Y[2][2], Yi[2][2];
-        so = gepp_step<4, 0>(R, Ri, Y, Yi);
-        dre = fma(Y[0][0], Y[1][1], -Y[0][1] * Y[1][0]);
-        dim = 0.0;
-    } else {
-        double R[4][4] = {{X[0][0], X[0][1], X[0][2], X[0][3]},
-                          {X[1][0], X[1][1], X[1][2], X[1][3]},
-                          {P.k13, -P.k14, P.k11 + H.h11r, H.h12r - P.k12},
-                          {P.k14, P.k24, H.h12r - P.k12, P.k22 + H.h22r}};
-        double Ri[4][4] = {{0.0, 0.0, 0.0, 0.0},
-                           {0.0, 0.0, 0.0, 0.0},
-                           {0.0, 0.0, H.h11i, H.h12i},
-                           {0.0, 0.0, H.h12i, H.h22i}};
-        double Y[2][2], Yi[2][2];
-        so = gepp_step<4, 2>(R, Ri, Y, Yi);
-        // det of the last complex 2x2
-        dre = fma(Y[0][0], Y[1][1], -Yi[0][0] * Yi[1][1]) -
-              fma(Y[0][1], Y[1][0], -Yi[0][1] * Yi[1][0]);
-        dim = fma(Y[0][0], Yi[1][1], Yi[0][0] * Y[1][1]) -
-              fma(Y[0][1], Yi[1][0], Yi[0][1] * Y[1][0]);
-    }
-    sgn ^= (unsigned)(__double2hiint(so.piv0) ^ __double2hiint(so.piv1));
-    kmin = min(kmin, min((unsigned)so.key0, (unsigned)so.key1));
-    kmax = max(kmax, max((unsigned)so.key0, (unsigned)so.key1));
-    perm ^= so.parity;
-    if (WANT_VALUE) {
-        acc.mul(so.piv0);
-        acc.mul(so.piv1);
-    }
-    kmax = max(kmax, max((unsigned)mag_key(dre), (unsigned)mag_key(dim)));
-    // A zero pivot (key 0: the pivot column is zero, det K = 0 exactly) makes every later
-    // pivot NaN through the unguarded reciprocal; it takes precedence, as in the oracle's
-    // elimination, which stops there with det = 0.  Inputs are finite and the range guard S9
-    // keeps every entry finite, so no Inf/NaN can precede a zero pivot.
-    const bool zero = (kmin == 0) || (dre == 0.0);
-    const bool bad = (kmax >= 0x7ff00000u) && (kmin != 0u);
-    const bool neg = (perm != 0) ^ ((sgn >> 31) != 0) ^ (dre < 0.0);
-
-    DetOut out;
-    out.bad = bad;
-    out.sign = zero ? 0 : (neg ? -1 : 1);
-    out.mre = 0.0;
-    out.mim = 0.0;
-    out.e2 = 0;
-    if (WANT_VALUE && kmin != 0) {
-        // value = (-1)^permutation * (prod pivots) * (dre + i dim)
-        const double ps = perm ? -acc.m : acc.m;
-        double re = ps * dre, im = ps * dim;
-        const double t = fmax(fabs(re), fabs(im));
-        if (t == 0.0 || !isfinite(t)) {
-            out.mre = re;
-            out.mim = im;
-            out.e2 = (t == 0.0) ? 0 : acc.e;
-        } else {
-            int ex;
-            frexp(t, &ex);
-            out.mre = ldexp(re, -ex);
-            out.mim = ldexp(im, -ex);
-            out.e2 = acc.e + ex;
-        }
-    }
-    return out;
+    return st.finish(hs());
 }
 
 // det K(k, c) for one row whose LayerConst[0..N] (k-scaled) and velocity list are in `lc`,

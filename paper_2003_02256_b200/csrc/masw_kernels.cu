@@ -537,35 +537,8 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             for (int half = 0; half < 2; ++half) {
                 unsigned pend = half ? pend1 : pend0;
                 unsigned found = 0;
-                while (pend) {
-                    const int r = half * 32 + __ffs(pend) - 1;
-                    pend &= pend - 1;
-                    const double k = lds_f64(ka + 8u * (unsigned)r);
-                    int s = 0;
-                    bool bad = false;
-                    if (valid) {
-                        const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
-                            N,
-                            [&](int e) {
-                                const unsigned o = 32u * (unsigned)e;
-                                return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
-                                                       lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
-                            },
-                            [&] {
-                                const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
-                                const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
-                                HsRoot h;
-                                h.r = rs.x;
-                                h.s = rs.y;
-                                h.gw = gt.x;
-                                h.t = gt.y;
-                                h.kase = lds_s32(hca + 32u);
-                                return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
-                            });
-                        s = d.sign;
-                        bad = d.bad;
-                        ++ev32;
-                    }
+                // first-sign-change bookkeeping of row r for this chunk (lane signs s, bad)
+                auto settle = [&](int r, int s, bool bad) {
                     int sprev = __shfl_up_sync(FULL, s, 1);
                     if (lane == 0) sprev = lds_s32(ya + 4u * (unsigned)r);
                     const bool ev = valid && (bad || (j > 0 && s != sprev));
@@ -589,6 +562,38 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                     } else if (lane == 31) {
                         sts_s32(ya + 4u * (unsigned)r, s);   // carried to the next chunk
                     }
+                };
+                auto hs_of = [&](double k) {
+                    const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
+                    const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
+                    HsRoot h;
+                    h.r = rs.x;
+                    h.s = rs.y;
+                    h.gw = gt.x;
+                    h.t = gt.y;
+                    h.kase = lds_s32(hca + 32u);
+                    return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
+                };
+                while (pend) {
+                    const int r = half * 32 + __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    const double k = lds_f64(ka + 8u * (unsigned)r);
+                    int s = 0;
+                    bool bad = false;
+                    if (valid) {
+                        const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
+                            N,
+                            [&](int e) {
+                                const unsigned o = 32u * (unsigned)e;
+                                return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
+                                                       lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
+                            },
+                            [&] { return hs_of(k); });
+                        s = d.sign;
+                        bad = d.bad;
+                        ++ev32;
+                    }
+                    settle(r, s, bad);
                 }
                 if (half) pend1 &= ~found; else pend0 &= ~found;
             }
