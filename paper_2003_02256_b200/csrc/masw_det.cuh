@@ -223,10 +223,10 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, uns
     double r = fma(md, -kExpD_hi, th);                     // exact (m kExpD_hi has <= 33 bits)
     r = fma(md, -c_k[1], r);
     const double u = r * r;
-    double pe = c_expE3[0];                                // E / r^2
-    double po = c_expO3[0];                                // O / r
+    double pe = fma(kExpE3_0, u, c_expE3[1]);              // E / r^2
+    double po = fma(kExpO3_0, u, c_expO3[1]);              // O / r
 #pragma unroll
-    for (int i = 1; i < 4; ++i) {
+    for (int i = 2; i < 4; ++i) {
         pe = fma(pe, u, c_expE3[i]);
         po = fma(po, u, c_expO3[i]);
     }

@@ -319,6 +319,24 @@ def test_models_kernel_bitwise_equals_row_kernel(masw, L):
     assert np.array_equal(rows[3], mm[3])
 
 
+@pytest.mark.parametrize("N", [1, 3, 7])
+def test_models_kernel_bitwise_any_depth(masw, N):
+    """Random N-layer ensembles (N = 7 is the deepest whose per-warp cache fits the one-CTA
+    layout): model-major and row kernels agree bitwise."""
+    rng = np.random.default_rng(N)
+    M = 150
+    h = rng.uniform(0.5, 4.0, (M, N))
+    beta = rng.uniform(60.0, 420.0, (M, N + 1))
+    alpha = np.full((M, N + 1), 1440.0)
+    rho = rng.uniform(1700.0, 2100.0, (M, N + 1))
+    lam = synth.geom(40.0, 1.0, 40)
+    c = synth.maswaves_grid()
+    a = masw.masw_curves_ensemble(h, alpha, beta, rho, lam, c, flags=masw.SCHED_ROWS)
+    b = masw.masw_curves_ensemble(h, alpha, beta, rho, lam, c, flags=masw.SCHED_MODELS)
+    assert a.status == b.status
+    assert np.array_equal(a.idx, b.idx) and np.array_equal(a.ct, b.ct, equal_nan=True)
+
+
 def test_models_kernel_oracle_parity(masw, orc):
     w = synth.workload("ensemble", M=150)
     mods = w.models
