@@ -683,6 +683,9 @@ int auto_team_warps(int64_t rows, int64_t V, int device)
     // (~ 16 TEAM / dets_per_row) with dets_per_row ~ V/2:  TEAM* = sqrt(Wres d / (32 R)).
     const int sms = sm_count(device);
     const double wres = sms * 16.0;   // resident warps: 2 CTAs x 8 warps per SM (launch bounds)
+    // with >= 4 rows per resident warp the tail is short anyway and one-warp teams waste the
+    // least speculation (measured: C4 2.35 ms at TEAM = 1 vs 2.45 ms at 2; C3 equal)
+    if ((double)rows >= 4.0 * wres) return 1;
     const double d = (double)V / 2.0;
     // halved: measured team optima on C3/C4 (1-2) sit below the bare tail/waste model (4),
     // which ignores the per-chunk team barriers
