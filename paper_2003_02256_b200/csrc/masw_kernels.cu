@@ -405,7 +405,10 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 #endif
 constexpr int kModelRows = 64;
 // 16 warps in ONE CTA per SM: one copy of the 64 KB cosh/sinh table serves all of them.
-constexpr int kModelsBlock = 512;
+#ifndef MASW_MODELS_BLOCK
+#define MASW_MODELS_BLOCK 512
+#endif
+constexpr int kModelsBlock = MASW_MODELS_BLOCK;
 
 // Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
 // velocities (S4), k per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
