@@ -337,6 +337,22 @@ def test_models_kernel_bitwise_any_depth(masw, N):
     assert np.array_equal(a.idx, b.idx) and np.array_equal(a.ct, b.ct, equal_nan=True)
 
 
+def test_models_kernel_s4_on_grid_velocities(masw, orc):
+    """The C2 model's layer velocities (75, 90, ..., 290 m/s) lie ON its velocity grid, so
+    the S4 perturbation fires inside the model-major kernel's warp-balloted check; 40 copies
+    (forced model-major) equal the oracle's C_t exactly and the row kernel bitwise."""
+    w = synth.workload("maswaves")
+    m = w.models
+    rep = lambda x: np.repeat(x, 40, axis=0)
+    h, al, be, rh = rep(m.h), rep(m.alpha), rep(m.beta), rep(m.rho)
+    mm = masw.masw_curves_ensemble(h, al, be, rh, w.lam, w.c, w.ce, flags=masw.SCHED_MODELS)
+    rr = masw.masw_curves_ensemble(h, al, be, rh, w.lam, w.c, w.ce, flags=masw.SCHED_ROWS)
+    ost, oct_, oidx, _ = orc.curve(*margs(m), w.lam, w.c)
+    assert np.array_equal(mm.idx, rr.idx)
+    assert all(np.array_equal(mm.idx[k], oidx) for k in range(40))
+    assert all(np.array_equal(mm.ct[k], oct_) for k in range(40))
+
+
 def test_models_kernel_oracle_parity(masw, orc):
     w = synth.workload("ensemble", M=150)
     mods = w.models
