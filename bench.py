@@ -292,9 +292,11 @@ def run_ours(args):
 
     # ---- warm-up (validated, synchronous calls); work counters and scan-kernel time
     alg_ref = None
+    fallbacks = None
     for _ in range(args.warmup):
         step_device(False)
         alg_ref, _ = masw.masw_last_work()
+        fallbacks = masw.masw_last_fallbacks()
         step_e2e()
     barrier()
 
@@ -394,6 +396,9 @@ def run_ours(args):
         "dets_per_step": total_dets / args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_tot_ms / args.steps},
+        "sign_method": {"scan": "certified block LDL^T recursion, banded GEPP where the "
+                                "multiplier certificate fails (DESIGN.md)",
+                        "gepp_fallback_dets_per_step_rank0": fallbacks},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

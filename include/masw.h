@@ -118,6 +118,10 @@ typedef struct {
  * element; runs the row scan (never the model-major one).  Applies to masw_curve,
  * masw_curves_ensemble and masw_det_grid. */
 #define MASW_STABLE 0x80u
+/* Scan signs by the banded GEPP for every determinant (default: the block LDL^T recursion,
+ * certified per determinant, GEPP only where the certificate fails; DESIGN.md "sign by
+ * block recursion").  For validation and A/B measurement; the results agree. */
+#define MASW_PIVOTED 0x100u
 
 /* Execution options; a NULL masw_exec means {device = current, stream = legacy default,
  * team_warps = 0 (auto), flags = 0}. */
@@ -200,6 +204,11 @@ int64_t masw_last_team_dets(int64_t *out, int64_t n);
  * are not counted for -2), and the determinants actually evaluated including speculation.
  * Only filled for synchronous calls (not MASW_ASYNC); -1 otherwise. */
 int masw_last_work(int64_t *algorithmic_dets, int64_t *evaluated_dets);
+
+/* Of the determinants the calling thread's last synchronous scan evaluated, how many had
+ * their sign re-evaluated by the banded GEPP because the block recursion's multipliers were
+ * not certified; -1 if there was no such call. */
+int64_t masw_last_fallbacks(void);
 
 #ifdef __cplusplus
 }

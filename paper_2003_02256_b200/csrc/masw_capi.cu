@@ -30,7 +30,7 @@ thread_local Workspace *t_pinned_ws = nullptr;   // pinned host copy target for 
 constexpr int kScanRing = 64;
 thread_local cudaEvent_t t_scan_ev[kScanRing][2] = {};
 thread_local long long t_scan_count = 0;   // TIME_SCAN launches recorded by this thread
-thread_local long long t_last_alg = -1, t_last_eval = -1;
+thread_local long long t_last_alg = -1, t_last_eval = -1, t_last_fb = -1;
 thread_local std::vector<long long> t_team_dets;
 thread_local long long t_team_count = -1;
 
@@ -225,7 +225,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         return MASW_E_ARG;
     if (misfit_out && !ce) return MASW_E_ARG;
     if (mod_in.M == 0) return MASW_OK;
-    t_last_alg = t_last_eval = -1;
+    t_last_alg = t_last_eval = t_last_fb = -1;
     const Exec ex = resolve(exp);
     if (ex.team != 0 && (ex.team < 1 || ex.team > 16 || (ex.team & (ex.team - 1))))
         return MASW_E_ARG;
@@ -268,7 +268,8 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         const int sched = (ex.flags & MASW_SCHED_CONTIGUOUS) ? 1 : ((ex.flags & MASW_SCHED_MODULAR) ? 2 : 0);
         const bool stable = (ex.flags & MASW_STABLE) != 0;
         ScanArgs sa{mod, dlam, L, dc, V, dct, didx, ws,
-                    (dce ? 0x7Fu : 0x1Fu) | (stable ? kGridStable : 0u), sched, nullptr, stable};
+                    (dce ? 0x7Fu : 0x1Fu) | (stable ? kGridStable : 0u), sched, nullptr, stable,
+                    (ex.flags & MASW_PIVOTED) != 0};
         // model-major scan for ensembles (auto unless a team size, a static schedule or
         // MASW_SCHED_ROWS is requested; MASW_SCHED_MODELS forces it where it fits)
         const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 && !stable &&
@@ -306,6 +307,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         if (code < 0) return code;
         t_last_alg = (long long)w.alg_dets;
         t_last_eval = (long long)w.eval_dets;
+        t_last_fb = (long long)w.fallback_dets;
         if (stats) {
             t_team_dets.assign((size_t)nteams, 0);
             CK(cudaMemcpy(t_team_dets.data(), sa.team_dets, nteams * sizeof(long long),
@@ -573,6 +575,8 @@ int64_t masw_last_team_dets(int64_t *out, int64_t n)
         for (int64_t i = 0; i < n && i < t_team_count; ++i) out[i] = t_team_dets[(size_t)i];
     return t_team_count;
 }
+
+int64_t masw_last_fallbacks(void) { return t_last_fb; }
 
 int masw_last_work(int64_t *algorithmic_dets, int64_t *evaluated_dets)
 {

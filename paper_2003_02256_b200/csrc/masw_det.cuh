@@ -996,6 +996,97 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
     return st.finish(hs());
 }
 
+// -------------------------------------------------------------- sign by block recursion
+// The scan needs only sgn(Re det K).  K is symmetric 2x2-block tridiagonal, so the block
+// LDL^T recursion  S_0 = A_0,  S_{t+1} = A_{t+1} - B_t^T S_t^{-1} B_t,  det K = prod det S_t
+// gives the sign with no pivot search, no branches and no row bookkeeping (~25 FP64 ops
+// per node, like one banded-GEPP step, but ~45 fewer integer / move / branch instructions).
+// Unpivoted elimination is backward stable when its multipliers W_t = S_t^{-1} B_t stay
+// bounded (threshold pivoting: then |L||U| <= (1 + |W|) |K| block-wise), so the sign is as
+// reliable as GEPP's; every step checks max|W_t| <= 2^kBlockMultExp (exponent arithmetic on
+// the high words) and that every det S_t is nonzero and finite.  A determinant that fails
+// the check (a leading block S_t nearly singular: rare, measured in DESIGN.md) is re-evaluated
+// by the caller with the banded GEPP (det_core), so the result always follows partial
+// pivoting where the unpivoted recursion is not certified.  (Reading S11: the values of
+// det K -- masw_det_grid, parity -- always come from the GEPP.)
+constexpr int kBlockMultExp = 12;   // multipliers up to 4096
+
+struct SignOut {
+    int sign;   // sgn(Re det K)
+    bool bad;   // non-finite (only from the GEPP re-evaluation)
+    bool ok;    // certified (else re-evaluate with GEPP)
+};
+
+// exponent field of |x| (0 for zero/denormal, 0x7ff for Inf/NaN)
+__device__ __forceinline__ int exp_of(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
+
+template <int UNROLL, class ElemFn, class HsFn>
+__device__ __forceinline__ SignOut det_sign_block(int N, ElemFn &&elem, HsFn &&hs)
+{
+    Elem P = elem(0);
+    double s11 = P.k11, s12 = P.k12, s22 = P.k22;   // S_0 = top block of layer 0
+    unsigned sgn = 0u;
+    int worst = -4096;    // max over steps of exponent(max|W'|) - exponent(det S)
+    int dmin = 0x7ff;     // min exponent of det S (0: zero/denormal)
+    int dmax = 0;         // max exponent of det S (0x7ff: Inf/NaN)
+
+    // eliminate the current node with block S and coupling B = [[b11, b12], [-b12, b22]]
+    // (layer P's k13, k14, k24); returns M = B^T S^{-1} B scaled back (m11, m12, m22)
+    auto eliminate = [&](double b11, double b12, double b22, double &m11, double &m12,
+                         double &m22) {
+        const double d = fma(s11, s22, -(s12 * s12));
+        // W' = adj(S) B, adj(S) = [[s22, -s12], [-s12, s11]], b21 = -b12
+        const double w11 = fma(s22, b11, s12 * b12);
+        const double w12 = fma(s22, b12, -s12 * b22);
+        const double w21 = fma(-s12, b11, -s11 * b12);
+        const double w22 = fma(-s12, b12, s11 * b22);
+        const double id = rcp_fast(d);
+        // M' = B^T W' (symmetric), M = M' / d
+        m11 = fma(b11, w11, -b12 * w21) * id;
+        m12 = fma(b11, w12, -b12 * w22) * id;
+        m22 = fma(b12, w12, b22 * w22) * id;
+        sgn ^= (unsigned)__double2hiint(d);
+        const int ed = exp_of(d);
+        const int ew = max(max(exp_of(w11), exp_of(w12)), max(exp_of(w21), exp_of(w22)));
+        worst = max(worst, ew - ed);
+        dmin = min(dmin, ed);
+        dmax = max(dmax, ed);
+    };
+
+    constexpr int kU = UNROLL;
+#pragma unroll kU
+    for (int t = 0; t + 1 < N; ++t) {
+        const Elem Q = elem(t + 1);
+        double m11, m12, m22;
+        eliminate(P.k13, P.k14, P.k24, m11, m12, m22);
+        // S_{t+1} = bottom(P) + top(Q) - M
+        s11 = (P.k11 + Q.k11) - m11;
+        s12 = (Q.k12 - P.k12) - m12;
+        s22 = (P.k22 + Q.k22) - m22;
+        P = Q;
+    }
+    const HalfSpace H = hs();
+    double m11, m12, m22;
+    eliminate(P.k13, P.k14, P.k24, m11, m12, m22);
+    // S_N = bottom(P) + K_hs - M (complex when c > beta_N)
+    const double r11 = (P.k11 + H.h11r) - m11, r12 = (H.h12r - P.k12) - m12,
+                 r22 = (P.k22 + H.h22r) - m22;
+    double dre;
+    if (H.real) {
+        dre = fma(r11, r22, -(r12 * r12));
+    } else {
+        // Re[(r11 + i h11i)(r22 + i h22i) - (r12 + i h12i)^2]
+        dre = fma(r11, r22, -H.h11i * H.h22i) - fma(r12, r12, -H.h12i * H.h12i);
+    }
+    const int ee = exp_of(dre);
+    SignOut o;
+    o.ok = (worst <= kBlockMultExp) && (dmin > 0) && (dmax < 0x7ff) && (ee < 0x7ff);
+    o.bad = false;
+    const bool neg = ((sgn >> 31) != 0) ^ (dre < 0.0);
+    o.sign = (dre == 0.0) ? 0 : (neg ? -1 : 1);
+    return o;
+}
+
 // det K(k, c) for one row whose LayerConst[0..N] (k-scaled) and velocity list are in `lc`,
 // `vel` (shared memory).  `maybe_near` = false means c is already the S4-perturbed velocity
 // (the scan resolves S4 per warp for its 32 velocities, see scan_kernel), which skips the

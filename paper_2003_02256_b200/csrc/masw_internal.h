@@ -21,6 +21,7 @@ struct Workspace {
     unsigned int row_status;           // bit0 some idx == -1, bit1 some idx == -2
     int abort;                         // set by the scan kernel when validation failed
     int range_bad;                     // k_max * h_max > 350
+    unsigned long long fallback_dets;  // sign re-evaluated with GEPP (block recursion not certified)
 };
 
 // Model classes for Workspace::model_err
@@ -46,6 +47,7 @@ struct ScanArgs {
     int sched;           // 0 work-stealing queue, 1 static contiguous, 2 static modular
     unsigned long long *team_dets;  // per-team algorithmic det counts (nullable)
     int stable;          // MASW_STABLE: the scaled, cancellation-free element (row kernel)
+    int pivoted;         // MASW_PIVOTED: every sign by the banded GEPP (no block recursion)
 };
 
 // grid_mask bit: the call uses the stable element, range guard k h <= 700 instead of 350

@@ -201,6 +201,20 @@ constexpr int scan_min_blocks()
     return BLOCK == 256 ? MASW_SCAN_MINB : 1;
 }
 
+// Sign of det K by the banded GEPP for one lane whose block-recursion sign was not certified
+// (det_sign_block); out of line so the hot loop's code stays small.  Returns -1/0/+1, or 2
+// for a non-finite determinant.
+#ifndef MASW_BLOCK_SIGN
+#define MASW_BLOCK_SIGN 1
+#endif
+template <bool STABLE>
+static __device__ __noinline__ int row_det_gepp(const LayerConst *lc, const double *vel,
+                                                unsigned ta, int N, double c)
+{
+    const DetOut d = det_K<false, 0, STABLE>(lc, vel, ta, N, c, false);
+    return d.bad ? 2 : d.sign;
+}
+
 template <int TEAM, int BLOCK, bool STABLE>
 __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(ScanArgs a)
 {
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     const int64_t M = a.mod.M, L = a.L, V = a.V;
     const int64_t rows = M * L;
     const double *__restrict__ cg = a.c;
-    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0;
+    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0, my_fb = 0;
     unsigned my_status = 0;
     int buf = 0;
     // static schedules (the paper's partitions): team g of G takes a
@@ -321,9 +335,34 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             int s = 0;
             bool bad = false;
             if (j < V) {
+#if MASW_BLOCK_SIGN
+                const double c2 = c * c;
+                SignOut so;
+                so.ok = false;
+                if (!a.pivoted)
+                    so = det_sign_block<1>(
+                        N,
+                        [&](int e) {
+                            if constexpr (STABLE) return layer_elem_stable(load_lc(lc + e), c2, ta);
+                            else return layer_elem(load_lc(lc + e), c2, ta);
+                        },
+                        [&] {
+                            const LayerConst H = load_lc(lc + N);
+                            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.mu);
+                        });
+                if (so.ok) {
+                    s = so.sign;
+                } else {
+                    const int r = row_det_gepp<STABLE>(lc, vel, ta, N, c);
+                    bad = (r == 2);
+                    s = bad ? 0 : r;
+                    my_fb += a.pivoted ? 0 : 1;
+                }
+#else
                 const DetOut d = det_K<false, 0, STABLE>(lc, vel, ta, N, c, false);
                 s = d.sign;
                 bad = d.bad;
+#endif
                 ++my_eval;
             }
             int sprev = __shfl_up_sync(FULL, s, 1);
@@ -383,10 +422,12 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     // ---- per-warp aggregation of the work counters (one atomic per warp)
     my_alg = warp_sum_u64(my_alg);
     my_eval = warp_sum_u64(my_eval);
+    my_fb = warp_sum_u64(my_fb);
     my_status = __reduce_or_sync(FULL, my_status);
     if (lane == 0) {
         if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
         if (my_eval) atomicAdd(&ws->eval_dets, my_eval);
+        if (my_fb) atomicAdd(&ws->fallback_dets, my_fb);
         if (my_status) atomicOr(&ws->row_status, my_status);
     }
 }
@@ -424,6 +465,33 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
                    32u * lane_cache_stride(N));                            // per-lane roots
 }
 
+// GEPP sign for one lane of the model-major kernel (see row_det_gepp); the same element
+// and half-space evaluation as the kernel's hot path.
+static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, unsigned ha,
+                                                   unsigned hca, unsigned ta, double k,
+                                                   double c2, int N)
+{
+    const DetOut d = det_core<false, 0, 1>(
+        N,
+        [&](int e) {
+            const unsigned o = 32u * (unsigned)e;
+            return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k, lds_v2(ca + o),
+                                   lds_v2(ca + o + 16u), c2, ta);
+        },
+        [&] {
+            const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
+            const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
+            HsRoot h;
+            h.r = rs.x;
+            h.s = rs.y;
+            h.gw = gt.x;
+            h.t = gt.y;
+            h.kase = lds_s32(hca + 32u);
+            return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
+        });
+    return d.bad ? 2 : d.sign;
+}
+
 __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -458,7 +526,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     const int64_t items = M * groups;
     const double *__restrict__ cg = a.c;
     const int nv = 2 * (N + 1);
-    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0;
+    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0, my_fb = 0;
     unsigned my_status = 0;
 
     for (;;) {
@@ -499,7 +567,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
         // rows of the item in two 32-bit halves: pending = not yet found
         unsigned pend0 = (nr >= 32) ? ~0u : ((1u << nr) - 1u);
         unsigned pend1 = (nr > 32) ? ((nr == 64) ? ~0u : ((1u << (nr - 32)) - 1u)) : 0u;
-        unsigned ev32 = 0;
+        unsigned ev32 = 0, fb32 = 0;
         for (int base = 0; base < V && (pend0 | pend1); base += 32) {
             const int j = base + lane;
             const bool valid = j < V;
@@ -584,6 +652,28 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                     int s = 0;
                     bool bad = false;
                     if (valid) {
+#if MASW_BLOCK_SIGN
+                        SignOut so;
+                        so.ok = false;
+                        if (!a.pivoted)
+                            so = det_sign_block<MASW_MODELS_UNROLL>(
+                                N,
+                                [&](int e) {
+                                    const unsigned o = 32u * (unsigned)e;
+                                    return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
+                                                           lds_v2(ca + o), lds_v2(ca + o + 16u), c2,
+                                                           ta);
+                                },
+                                [&] { return hs_of(k); });
+                        if (so.ok) {
+                            s = so.sign;
+                        } else {
+                            const int r = models_det_gepp(ma, ca, ha, hca, ta, k, c2, N);
+                            bad = (r == 2);
+                            s = bad ? 0 : r;
+                            fb32 += a.pivoted ? 0u : 1u;
+                        }
+#else
                         const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
                             N,
                             [&](int e) {
@@ -594,6 +684,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                             [&] { return hs_of(k); });
                         s = d.sign;
                         bad = d.bad;
+#endif
                         ++ev32;
                     }
                     settle(r, s, bad);
@@ -603,6 +694,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             __syncwarp();   // the next chunk rewrites this lane's roots; carries are visible
         }
         my_eval += ev32;
+        my_fb += fb32;
         for (int half = 0; half < 2; ++half) {
             for (unsigned pend = half ? pend1 : pend0; pend; pend &= pend - 1) {
                 const int r = half * 32 + __ffs(pend) - 1;
@@ -623,10 +715,12 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
 
     my_alg = warp_sum_u64(my_alg);
     my_eval = warp_sum_u64(my_eval);
+    my_fb = warp_sum_u64(my_fb);
     my_status = __reduce_or_sync(FULL, my_status);
     if (lane == 0) {
         if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
         if (my_eval) atomicAdd(&ws->eval_dets, my_eval);
+        if (my_fb) atomicAdd(&ws->fallback_dets, my_fb);
         if (my_status) atomicOr(&ws->row_status, my_status);
     }
 }

@@ -25,6 +25,7 @@ ASYNC, TIME_SCAN = 0x1, 0x2
 SCHED_CONTIGUOUS, SCHED_MODULAR, TEAM_STATS = 0x4, 0x8, 0x10
 SCHED_ROWS, SCHED_MODELS = 0x20, 0x40   # force the row / model-major scan kernel
 STABLE = 0x80   # cancellation-free, exponentially scaled element (f3), k h <= 700
+PIVOTED = 0x100   # every scan sign by the banded GEPP (validation / A-B)
 MAX_LAYERS = 64
 
 
@@ -84,6 +85,8 @@ def lib():
         L.masw_last_team_dets.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]
         L.masw_recent_scan_ms.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int32]
         L.masw_last_work.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+        L.masw_last_fallbacks.restype = ctypes.c_int64
+        L.masw_last_fallbacks.argtypes = []
         L.masw_probe_fp64_peak.argtypes = [ctypes.c_int32, ctypes.c_double,
                                            ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double)]
@@ -287,6 +290,11 @@ def masw_last_team_dets():
     out = np.zeros(n, dtype=np.int64)
     lib().masw_last_team_dets(out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n)
     return out
+
+
+def masw_last_fallbacks() -> int:
+    """Determinants of the last synchronous scan re-evaluated with partial pivoting."""
+    return int(lib().masw_last_fallbacks())
 
 
 def masw_last_work():

@@ -56,9 +56,10 @@ def main():
             t = time_call(fn)
             alg, ev = masw.masw_last_work()
             kms = masw.masw_last_scan_ms()
+            fb = masw.masw_last_fallbacks()
             print(f"{name:10s} team={team:2d} call {t:9.3f} ms  scan {kms:9.3f} ms  "
-                  f"alg {alg:12d} eval {ev:12d}  {alg / (kms * 1e-3) / 1e9:8.3f} Gdet/s",
-                  flush=True)
+                  f"alg {alg:12d} eval {ev:12d} gepp-fallback {fb:9d}  "
+                  f"{alg / (kms * 1e-3) / 1e9:8.3f} Gdet/s", flush=True)
 
 
 if __name__ == "__main__":

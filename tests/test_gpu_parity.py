@@ -353,6 +353,39 @@ def test_models_kernel_s4_on_grid_velocities(masw, orc):
     assert all(np.array_equal(mm.ct[k], oct_) for k in range(40))
 
 
+def test_block_sign_vs_pivoted_ensemble(masw, orc):
+    """The scan's default sign (certified block LDL^T recursion, GEPP where uncertified) and
+    the all-GEPP scan (MASW_PIVOTED) give the same first sign changes on 20k C5 models
+    (800k rows); any difference would have to be a near-root row the parity rule allows.
+    The GEPP fallback fires (it is exercised) but rarely."""
+    w = synth.workload("ensemble", M=20_000)
+    mods = w.models
+    args = [dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)] + [dev(w.lam), dev(w.c)]
+    a = masw.masw_curves_ensemble(*args, dev(w.ce))
+    fb = masw.masw_last_fallbacks()
+    alg, ev = masw.masw_last_work()
+    b = masw.masw_curves_ensemble(*args, dev(w.ce), flags=masw.PIVOTED)
+    ia, ib = a.idx.cpu().numpy(), b.idx.cpu().numpy()
+    diff = np.argwhere(ia != ib)
+    assert len(diff) <= 2, len(diff)
+    for m, i in diff:
+        mm = mods.take([m])
+        ok, exact, one = parity.ct_acceptable(orc, margs(mm), w.lam[i:i + 1], w.c,
+                                              ia[m, i:i + 1], ib[m, i:i + 1])
+        assert ok.all(), (m, i)
+    assert 0 < fb < 1e-4 * ev, (fb, ev)
+
+
+def test_block_sign_vs_pivoted_single_curves(masw):
+    """Row kernel: C2 and C4 curves identical under both sign methods."""
+    for name in ("maswaves", "realistic"):
+        w = synth.workload(name)
+        a = [dev(x) for x in margs(w.models)] + [dev(w.lam), dev(w.c)]
+        s1, c1, i1 = masw.masw_curve(*a)
+        s2, c2, i2 = masw.masw_curve(*a, flags=masw.PIVOTED)
+        assert s1 == s2 and np.array_equal(i1.cpu().numpy(), i2.cpu().numpy()), name
+
+
 def test_models_kernel_oracle_parity(masw, orc):
     w = synth.workload("ensemble", M=150)
     mods = w.models
