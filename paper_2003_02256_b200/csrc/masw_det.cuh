@@ -600,6 +600,43 @@ __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, d
     return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, krho, krho * M.mu, c2);
 }
 
+// Elements of layer M for two wavenumbers ka, kb (two wavelengths of one model) at the same
+// velocity: one branch on the wave types, both rows' waves interleaved inside it.  Each
+// row's arithmetic is exactly layer_elem_root's (bitwise-identical elements).
+__device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka, double kb,
+                                                 double2 a, double2 b, double c2, unsigned tab,
+                                                 Elem &Ea, Elem &Eb)
+{
+    const double kha = ka * M.kh, khb = kb * M.kh;
+    const double kra = ka * M.krho, krb = kb * M.krho;
+    double Cra, XSra, SXra, Csa, XSsa, SXsa;
+    double Crb, XSrb, SXrb, Csb, XSsb, SXsb;
+    if (a.x > 0.0) {
+        if (b.x > 0.0) {
+            wave_hyp_root(a.x, a.y, kha, Cra, XSra, SXra, tab);
+            wave_hyp_root(a.x, a.y, khb, Crb, XSrb, SXrb, tab);
+            wave_hyp_root(b.x, b.y, kha, Csa, XSsa, SXsa, tab);
+            wave_hyp_root(b.x, b.y, khb, Csb, XSsb, SXsb, tab);
+        } else {
+            wave_hyp_root(a.x, a.y, kha, Cra, XSra, SXra, tab);
+            wave_hyp_root(a.x, a.y, khb, Crb, XSrb, SXrb, tab);
+            wave_trig_root(b.x, b.y, kha, Csa, XSsa, SXsa);
+            wave_trig_root(b.x, b.y, khb, Csb, XSsb, SXsb);
+        }
+    } else {
+        double t[6];
+        const double qa = fma(-c2, M.ia2, 1.0), qb = fma(-c2, M.ib2, 1.0);
+        waves_general(qa, qb, kha, t, tab);
+        Cra = t[0]; XSra = t[1]; SXra = t[2];
+        Csa = t[3]; XSsa = t[4]; SXsa = t[5];
+        waves_general(qa, qb, khb, t, tab);
+        Crb = t[0]; XSrb = t[1]; SXrb = t[2];
+        Csb = t[3]; XSsb = t[4]; SXsb = t[5];
+    }
+    Ea = elem_from_triples(Cra, XSra, SXra, Csa, XSsa, SXsa, kra, kra * M.mu, c2);
+    Eb = elem_from_triples(Crb, XSrb, SXrb, Csb, XSsb, SXsb, krb, krb * M.mu, c2);
+}
+
 // Half-space element K_hs = mu [[r w/(1-rs), w/(1-rs) - 2], [., s w/(1-rs)]], w = 1 - s^2 =
 // c^2/beta_N^2 (real), mu = k rho_N beta_N^2; cases by the branch of r, s (reading S3).
 // Split into the k-free factors (HsRoot: the roots, gw = w/(1 - r s) or its analogue, and
@@ -1020,20 +1057,31 @@ struct SignOut {
 // exponent field of |x| (0 for zero/denormal, 0x7ff for Inf/NaN)
 __device__ __forceinline__ int exp_of(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
-template <int UNROLL, class ElemFn, class HsFn>
-__device__ __forceinline__ SignOut det_sign_block(int N, ElemFn &&elem, HsFn &&hs)
-{
-    Elem P = elem(0);
-    double s11 = P.k11, s12 = P.k12, s22 = P.k22;   // S_0 = top block of layer 0
-    unsigned sgn = 0u;
-    int worst = -4096;    // max over steps of exponent(max|W'|) - exponent(det S)
-    int dmin = 0x7ff;     // min exponent of det S (0: zero/denormal)
-    int dmax = 0;         // max exponent of det S (0x7ff: Inf/NaN)
+// State of one block-recursion sign evaluation (see det_sign_block).
+struct BlockSign {
+    Elem P;                 // the previous layer's element
+    double s11, s12, s22;   // current leading block S_t (symmetric)
+    unsigned sgn;           // XOR of the det S_t sign bits
+    int worst;              // max over steps of exponent(max|W'|) - exponent(det S)
+    int dmin, dmax;         // min / max exponent of det S (0: zero/denormal, 0x7ff: Inf/NaN)
+
+    __device__ __forceinline__ void init(const Elem &E)
+    {
+        P = E;
+        s11 = E.k11;   // S_0 = top block of layer 0
+        s12 = E.k12;
+        s22 = E.k22;
+        sgn = 0u;
+        worst = -4096;
+        dmin = 0x7ff;
+        dmax = 0;
+    }
 
     // eliminate the current node with block S and coupling B = [[b11, b12], [-b12, b22]]
-    // (layer P's k13, k14, k24); returns M = B^T S^{-1} B scaled back (m11, m12, m22)
-    auto eliminate = [&](double b11, double b12, double b22, double &m11, double &m12,
-                         double &m22) {
+    // (layer P's k13, k14, k24): M = B^T S^{-1} B
+    __device__ __forceinline__ void eliminate(double &m11, double &m12, double &m22)
+    {
+        const double b11 = P.k13, b12 = P.k14, b22 = P.k24;
         const double d = fma(s11, s22, -(s12 * s12));
         // W' = adj(S) B, adj(S) = [[s22, -s12], [-s12, s11]], b21 = -b12
         const double w11 = fma(s22, b11, s12 * b12);
@@ -1051,40 +1099,79 @@ __device__ __forceinline__ SignOut det_sign_block(int N, ElemFn &&elem, HsFn &&h
         worst = max(worst, ew - ed);
         dmin = min(dmin, ed);
         dmax = max(dmax, ed);
-    };
+    }
 
-    constexpr int kU = UNROLL;
-#pragma unroll kU
-    for (int t = 0; t + 1 < N; ++t) {
-        const Elem Q = elem(t + 1);
+    // one node: S_{t+1} = bottom(P) + top(Q) - B^T S_t^{-1} B
+    __device__ __forceinline__ void step(const Elem &Q)
+    {
         double m11, m12, m22;
-        eliminate(P.k13, P.k14, P.k24, m11, m12, m22);
-        // S_{t+1} = bottom(P) + top(Q) - M
+        eliminate(m11, m12, m22);
         s11 = (P.k11 + Q.k11) - m11;
         s12 = (Q.k12 - P.k12) - m12;
         s22 = (P.k22 + Q.k22) - m22;
         P = Q;
     }
-    const HalfSpace H = hs();
-    double m11, m12, m22;
-    eliminate(P.k13, P.k14, P.k24, m11, m12, m22);
-    // S_N = bottom(P) + K_hs - M (complex when c > beta_N)
-    const double r11 = (P.k11 + H.h11r) - m11, r12 = (H.h12r - P.k12) - m12,
-                 r22 = (P.k22 + H.h22r) - m22;
-    double dre;
-    if (H.real) {
-        dre = fma(r11, r22, -(r12 * r12));
-    } else {
-        // Re[(r11 + i h11i)(r22 + i h22i) - (r12 + i h12i)^2]
-        dre = fma(r11, r22, -H.h11i * H.h22i) - fma(r12, r12, -H.h12i * H.h12i);
+
+    // last node: S_N = bottom(P) + K_hs - M (complex when c > beta_N); sign of Re det K
+    __device__ __forceinline__ SignOut finish(const HalfSpace &H)
+    {
+        double m11, m12, m22;
+        eliminate(m11, m12, m22);
+        const double r11 = (P.k11 + H.h11r) - m11, r12 = (H.h12r - P.k12) - m12,
+                     r22 = (P.k22 + H.h22r) - m22;
+        double dre;
+        if (H.real) {
+            dre = fma(r11, r22, -(r12 * r12));
+        } else {
+            // Re[(r11 + i h11i)(r22 + i h22i) - (r12 + i h12i)^2]
+            dre = fma(r11, r22, -H.h11i * H.h22i) - fma(r12, r12, -H.h12i * H.h12i);
+        }
+        SignOut o;
+        o.ok = (worst <= kBlockMultExp) && (dmin > 0) && (dmax < 0x7ff) && (exp_of(dre) < 0x7ff);
+        o.bad = false;
+        const bool neg = ((sgn >> 31) != 0) ^ (dre < 0.0);
+        o.sign = (dre == 0.0) ? 0 : (neg ? -1 : 1);
+        return o;
     }
-    const int ee = exp_of(dre);
-    SignOut o;
-    o.ok = (worst <= kBlockMultExp) && (dmin > 0) && (dmax < 0x7ff) && (ee < 0x7ff);
-    o.bad = false;
-    const bool neg = ((sgn >> 31) != 0) ^ (dre < 0.0);
-    o.sign = (dre == 0.0) ? 0 : (neg ? -1 : 1);
-    return o;
+};
+
+template <int UNROLL, class ElemFn, class HsFn>
+__device__ __forceinline__ SignOut det_sign_block(int N, ElemFn &&elem, HsFn &&hs)
+{
+    BlockSign st;
+    st.init(elem(0));
+    constexpr int kU = UNROLL;
+#pragma unroll kU
+    for (int t = 0; t + 1 < N; ++t) st.step(elem(t + 1));
+    return st.finish(hs());
+}
+
+// Two signs whose element evaluations share every branch (two wavelengths of one model at
+// the same velocity): with the branch-free block recursion the two evaluations interleave
+// completely (twice the instruction-level parallelism).
+template <int UNROLL, class Elem2Fn, class Hs2Fn>
+__device__ __forceinline__ void det_sign_block_pair(int N, Elem2Fn &&elem2, Hs2Fn &&hs2,
+                                                    SignOut &oa, SignOut &ob)
+{
+    BlockSign A, B;
+    {
+        Elem ea, eb;
+        elem2(0, ea, eb);
+        A.init(ea);
+        B.init(eb);
+    }
+    constexpr int kU = UNROLL;
+#pragma unroll kU
+    for (int t = 0; t + 1 < N; ++t) {
+        Elem qa, qb;
+        elem2(t + 1, qa, qb);
+        A.step(qa);
+        B.step(qb);
+    }
+    HalfSpace ha, hb;
+    hs2(ha, hb);
+    oa = A.finish(ha);
+    ob = B.finish(hb);
 }
 
 // det K(k, c) for one row whose LayerConst[0..N] (k-scaled) and velocity list are in `lc`,
