@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
                 SignOut so;
                 so.ok = false;
                 if (!a.pivoted)
-                    so = det_sign_block<1>(
+                    so = det_sign_block<MASW_LAYER_UNROLL>(
                         N,
                         [&](int e) {
                             if constexpr (STABLE) return layer_elem_stable(load_lc(lc + e), c2, ta);
