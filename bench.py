@@ -403,7 +403,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches / args.steps,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": kern_name + " (fused assemble + banded GEPP det + ballot scan)",
+                     "kernel": kern_name + " (fused assembly + certified block-recursion sign, GEPP fallback, ballot scan)",
                      "kernel_ms": kern_ms, "flops_per_det": F,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz "
                                     "(B200_PROFILING.md counts; MEASURED_PEAKS.json has no FP64)",
