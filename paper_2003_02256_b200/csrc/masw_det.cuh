@@ -1078,8 +1078,9 @@ struct BlockSign {
     }
 
     // eliminate the current node with block S and coupling B = [[b11, b12], [-b12, b22]]
-    // (layer P's k13, k14, k24): M = B^T S^{-1} B
-    __device__ __forceinline__ void eliminate(double &m11, double &m12, double &m22)
+    // (layer P's k13, k14, k24): M' = B^T adj(S) B and 1/det S (M = M' / det S is applied by
+    // the callers inside their subtraction, one fused operation per entry)
+    __device__ __forceinline__ void eliminate(double &m11, double &m12, double &m22, double &id)
     {
         const double b11 = P.k13, b12 = P.k14, b22 = P.k24;
         const double d = fma(s11, s22, -(s12 * s12));
@@ -1088,11 +1089,11 @@ struct BlockSign {
         const double w12 = fma(s22, b12, -s12 * b22);
         const double w21 = fma(-s12, b11, -s11 * b12);
         const double w22 = fma(-s12, b12, s11 * b22);
-        const double id = rcp_fast(d);
-        // M' = B^T W' (symmetric), M = M' / d
-        m11 = fma(b11, w11, -b12 * w21) * id;
-        m12 = fma(b11, w12, -b12 * w22) * id;
-        m22 = fma(b12, w12, b22 * w22) * id;
+        id = rcp_fast(d);
+        // M' = B^T W' (symmetric)
+        m11 = fma(b11, w11, -b12 * w21);
+        m12 = fma(b11, w12, -b12 * w22);
+        m22 = fma(b12, w12, b22 * w22);
         sgn ^= (unsigned)__double2hiint(d);
         const int ed = exp_of(d);
         const int ew = max(max(exp_of(w11), exp_of(w12)), max(exp_of(w21), exp_of(w22)));
@@ -1104,21 +1105,21 @@ struct BlockSign {
     // one node: S_{t+1} = bottom(P) + top(Q) - B^T S_t^{-1} B
     __device__ __forceinline__ void step(const Elem &Q)
     {
-        double m11, m12, m22;
-        eliminate(m11, m12, m22);
-        s11 = (P.k11 + Q.k11) - m11;
-        s12 = (Q.k12 - P.k12) - m12;
-        s22 = (P.k22 + Q.k22) - m22;
+        double m11, m12, m22, id;
+        eliminate(m11, m12, m22, id);
+        s11 = fma(-m11, id, P.k11 + Q.k11);
+        s12 = fma(-m12, id, Q.k12 - P.k12);
+        s22 = fma(-m22, id, P.k22 + Q.k22);
         P = Q;
     }
 
     // last node: S_N = bottom(P) + K_hs - M (complex when c > beta_N); sign of Re det K
     __device__ __forceinline__ SignOut finish(const HalfSpace &H)
     {
-        double m11, m12, m22;
-        eliminate(m11, m12, m22);
-        const double r11 = (P.k11 + H.h11r) - m11, r12 = (H.h12r - P.k12) - m12,
-                     r22 = (P.k22 + H.h22r) - m22;
+        double m11, m12, m22, id;
+        eliminate(m11, m12, m22, id);
+        const double r11 = fma(-m11, id, P.k11 + H.h11r), r12 = fma(-m12, id, H.h12r - P.k12),
+                     r22 = fma(-m22, id, P.k22 + H.h22r);
         double dre;
         if (H.real) {
             dre = fma(r11, r22, -(r12 * r12));
