@@ -1102,14 +1102,24 @@ struct BlockSign {
         dmax = max(dmax, ed);
     }
 
-    // one node: S_{t+1} = bottom(P) + top(Q) - B^T S_t^{-1} B
-    __device__ __forceinline__ void step(const Elem &Q)
+    // one node, in two halves so that the previous element P is dead before the next one is
+    // computed (no loop-carried copies of P, fewer live registers during the element):
+    //   pre():   T = bottom(P) - B^T S_t^{-1} B      (needs S_t and P only)
+    //   post(Q): S_{t+1} = T + top(Q),  P = Q
+    double t11, t12, t22;
+    __device__ __forceinline__ void pre()
     {
         double m11, m12, m22, id;
         eliminate(m11, m12, m22, id);
-        s11 = fma(-m11, id, P.k11 + Q.k11);
-        s12 = fma(-m12, id, Q.k12 - P.k12);
-        s22 = fma(-m22, id, P.k22 + Q.k22);
+        t11 = fma(-m11, id, P.k11);
+        t12 = fma(-m12, id, -P.k12);
+        t22 = fma(-m22, id, P.k22);
+    }
+    __device__ __forceinline__ void post(const Elem &Q)
+    {
+        s11 = t11 + Q.k11;
+        s12 = t12 + Q.k12;
+        s22 = t22 + Q.k22;
         P = Q;
     }
 
@@ -1143,7 +1153,10 @@ __device__ __forceinline__ SignOut det_sign_block(int N, ElemFn &&elem, HsFn &&h
     st.init(elem(0));
     constexpr int kU = UNROLL;
 #pragma unroll kU
-    for (int t = 0; t + 1 < N; ++t) st.step(elem(t + 1));
+    for (int t = 0; t + 1 < N; ++t) {
+        st.pre();
+        st.post(elem(t + 1));
+    }
     return st.finish(hs());
 }
 
@@ -1164,10 +1177,12 @@ __device__ __forceinline__ void det_sign_block_pair(int N, Elem2Fn &&elem2, Hs2F
     constexpr int kU = UNROLL;
 #pragma unroll kU
     for (int t = 0; t + 1 < N; ++t) {
+        A.pre();
+        B.pre();
         Elem qa, qb;
         elem2(t + 1, qa, qb);
-        A.step(qa);
-        B.step(qb);
+        A.post(qa);
+        B.post(qb);
     }
     HalfSpace ha, hb;
     hs2(ha, hb);
