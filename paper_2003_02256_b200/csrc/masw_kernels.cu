@@ -441,9 +441,10 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 // shared memory, and reuses them for every active row -- each row's determinant then needs
 // only its k h_e-dependent part.  Results are those of scan_kernel (same algorithm per row,
 // K^ = K / k has the sign of K).
-// Two wavelengths per lane with fully interleaved (branch-free) sign evaluations, 12 warps
-// per SM at up to 168 registers: measured 47.9 ms vs 49.3 ms for one wavelength per lane
-// at 16 warps (C5); the node loop is then best not unrolled.
+// Two wavelengths per lane with fully interleaved (branch-free) sign evaluations, 16 warps
+// per SM at 128 registers (76 B of spills): measured on C5 45.7 ms vs 46.9 ms at 12 warps
+// (164 registers, no spills) and 46.9 ms for one wavelength per lane; the node loop is best
+// not unrolled (58.5 ms unrolled twice).
 #ifndef MASW_MODELS_PAIR
 #define MASW_MODELS_PAIR 1
 #endif
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 constexpr int kModelRows = 64;
 // ONE CTA per SM: one copy of the 64 KB cosh/sinh table serves all of its warps.
 #ifndef MASW_MODELS_BLOCK
-#define MASW_MODELS_BLOCK 384
+#define MASW_MODELS_BLOCK 512
 #endif
 constexpr int kModelsBlock = MASW_MODELS_BLOCK;
 
