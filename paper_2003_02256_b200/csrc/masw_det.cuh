@@ -573,15 +573,15 @@ __device__ __forceinline__ void wave_trig_root(double xneg, double rx, double kh
     SX = sn * rx;
 }
 
-// Element of layer M at wavenumber k from the cached roots a (P wave) and b (S wave).  M holds
-// the model's k-free constants: M.kh = h, M.krho = rho, M.mu = beta^2 (k h, k rho and
-// mu = (k rho) beta^2 are formed here exactly as the row scan's LayerConst fill forms them).
+// Element of K / k for layer M at wavenumber k from the cached roots a (P wave) and b (S wave).
+// M holds the model's k-free constants: M.kh = h, M.krho = rho, M.mu = rho beta^2; only
+// k h = k * M.kh depends on the wavelength (formed exactly as the row scan's LayerConst
+// fill forms it, so both scans compute bitwise-identical elements).
 __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, double2 a,
                                                 double2 b, double c2,
                                                 unsigned tab)
 {
     const double kh = k * M.kh;
-    const double krho = k * M.krho;
     double Cr, XSr, SXr, Cs, XSs, SXs;
     if (a.x > 0.0) {
         if (b.x > 0.0) {
@@ -597,7 +597,7 @@ __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, d
         Cr = t[0]; XSr = t[1]; SXr = t[2];
         Cs = t[3]; XSs = t[4]; SXs = t[5];
     }
-    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, krho, krho * M.mu, c2);
+    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, M.krho, M.mu, c2);
 }
 
 // Elements of layer M for two wavenumbers ka, kb (two wavelengths of one model) at the same
@@ -608,7 +608,6 @@ __device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka,
                                                  Elem &Ea, Elem &Eb)
 {
     const double kha = ka * M.kh, khb = kb * M.kh;
-    const double kra = ka * M.krho, krb = kb * M.krho;
     double Cra, XSra, SXra, Csa, XSsa, SXsa;
     double Crb, XSrb, SXrb, Csb, XSsb, SXsb;
     if (a.x > 0.0) {
@@ -633,8 +632,8 @@ __device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka,
         Crb = t[0]; XSrb = t[1]; SXrb = t[2];
         Csb = t[3]; XSsb = t[4]; SXsb = t[5];
     }
-    Ea = elem_from_triples(Cra, XSra, SXra, Csa, XSsa, SXsa, kra, kra * M.mu, c2);
-    Eb = elem_from_triples(Crb, XSrb, SXrb, Csb, XSsb, SXsb, krb, krb * M.mu, c2);
+    Ea = elem_from_triples(Cra, XSra, SXra, Csa, XSsa, SXsa, M.krho, M.mu, c2);
+    Eb = elem_from_triples(Crb, XSrb, SXrb, Csb, XSsb, SXsb, M.krho, M.mu, c2);
 }
 
 // Half-space element K_hs = mu [[r w/(1-rs), w/(1-rs) - 2], [., s w/(1-rs)]], w = 1 - s^2 =

@@ -291,11 +291,14 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             const double be = a.mod.beta[m * (N + 1) + e];
             const double rh = a.mod.rho[m * (N + 1) + e];
             LayerConst x;
+            // K / k (every entry of K is k times a function of k h and c, so det K =
+            // k^(2(N+1)) det(K/k): same sign).  The scans use these k-free constants; only
+            // k h carries the wavelength (det_grid_kernel, which returns values, keeps k).
             x.kh = (e < N) ? k * a.mod.h[m * N + e] : 0.0;
             x.ia2 = 1.0 / (al * al);
             x.ib2 = 1.0 / (be * be);
-            x.krho = k * rh;
-            x.mu = x.krho * (be * be);   // (k rho) beta^2, as layer_elem_root forms it
+            x.krho = rh;
+            x.mu = rh * (be * be);
             x.pad = 0.0;
             lc[e] = x;
             vel[2 * e] = al;
@@ -487,14 +490,13 @@ static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, uns
         },
         [&] {
             const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
-            const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
             HsRoot h;
             h.r = rs.x;
             h.s = rs.y;
             h.gw = gt.x;
             h.t = gt.y;
             h.kase = lds_s32(hca + 32u);
-            return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
+            return halfspace_k(h, lds_f64(ha + 32u));   // rho_N beta_N^2 (K / k)
         });
     return d.bad ? 2 : d.sign;
 }
@@ -554,8 +556,8 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             x.kh = (e < N) ? a.mod.h[m * N + e] : 0.0;
             x.ia2 = 1.0 / (al * al);
             x.ib2 = 1.0 / (be * be);
-            x.krho = rh;
-            x.mu = be * be;
+            x.krho = rh;               // K / k: rho and rho beta^2 (see scan_kernel)
+            x.mu = rh * (be * be);
             x.pad = 0.0;
             mc[e] = x;
             vel[2 * e] = al;
@@ -643,14 +645,13 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                 };
                 auto hs_of = [&](double k) {
                     const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
-                    const double2 hk = lds_v2(ha + 16u);   // (ib2, rho_N)
-                    HsRoot h;
+                            HsRoot h;
                     h.r = rs.x;
                     h.s = rs.y;
                     h.gw = gt.x;
                     h.t = gt.y;
                     h.kase = lds_s32(hca + 32u);
-                    return halfspace_k(h, (k * hk.y) * lds_f64(ha + 32u));
+                    return halfspace_k(h, lds_f64(ha + 32u));   // rho_N beta_N^2 (K / k)
                 };
                 while (pend) {
                     const int r = half * 32 + __ffs(pend) - 1;
