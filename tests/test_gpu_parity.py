@@ -355,10 +355,10 @@ def test_models_kernel_s4_on_grid_velocities(masw, orc):
 
 def test_block_sign_vs_pivoted_ensemble(masw, orc):
     """The scan's default sign (certified block LDL^T recursion, GEPP where uncertified) and
-    the all-GEPP scan (MASW_PIVOTED) give the same first sign changes on 20k C5 models
-    (800k rows); any difference would have to be a near-root row the parity rule allows.
-    The GEPP fallback fires (it is exercised) but rarely."""
-    w = synth.workload("ensemble", M=20_000)
+    the all-GEPP scan (MASW_PIVOTED) give the same first sign changes on the whole C5 bench
+    workload (100k models, 4M rows); any difference would have to be a near-root row the
+    parity rule allows.  The GEPP fallback fires (it is exercised) but rarely."""
+    w = synth.workload("ensemble", M=100_000)
     mods = w.models
     args = [dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)] + [dev(w.lam), dev(w.c)]
     a = masw.masw_curves_ensemble(*args, dev(w.ce))
