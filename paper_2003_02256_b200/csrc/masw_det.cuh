@@ -202,12 +202,6 @@ __device__ __forceinline__ void sqrt_rsqrt(double q, double &x, double &rx)
     x = q * rx;
 }
 
-// x * 2^k by exponent arithmetic (no overflow/underflow for the ranges used here).
-__device__ __forceinline__ double scale2(double x, int k)
-{
-    return __hiloint2double(__double2hiint(x) + (k << 20), __double2loint(x));
-}
-
 // cosh and sinh of th in [0, 350] (the range guard S9 bounds k h_e by 350 and x <= 1).
 // th = m d + r with d = ln2/8, |r| <= ln2/16; with A = cosh(m d), B = sinh(m d) from the
 // table and E = cosh r - 1, O = sinh r (near-minimax degree-3 polynomials in r^2, rel. err
