@@ -89,22 +89,20 @@ constexpr double kShifter = 6755399441055744.0;         // 1.5 * 2^52: round-to-
 // Split constants whose leading part has <= 21 significant bits (low word zero), so the
 // leading part is an instruction immediate (no register materialisation) and n * part is
 // exact for the n that occur; the trailing parts come from the constant bank (c_k).
-constexpr double kPio2Hi = 1.570796012878418;           // pi/2 = kPio2Hi + c_k[3] + c_k[4]
-static __constant__ double c_k[6] = {
-    kExpInvD,                  // 0: 8 / ln 2 (cosh/sinh reduction step d = ln2/8)
-    kExpD_lo,                  // 1: d - kExpD_hi
-    0.6366197723675814,        // 2: 2 / pi
-    3.139164786504813e-07,     // 3: pi/2 - kPio2Hi (53 bits)
-    1.0562999066987428e-23,    // 4: the rest (residual 5e-40)
-    0.375,                     // 5: rsqrt correction coefficient
+constexpr double kPio2Hi = 1.570796012878418;           // pi/2 = kPio2Hi + c_k[1] + c_k[2]
+static __constant__ double c_k[4] = {
+    0.6366197723675814,        // 0: 2 / pi
+    3.139164786504813e-07,     // 1: pi/2 - kPio2Hi (53 bits)
+    1.0562999066987428e-23,    // 2: the rest (residual 5e-40)
+    0.375,                     // 3: rsqrt correction coefficient
 };
 
 // cosh/sinh reconstruction table (masw_exp_table.h, generated, correctly rounded): a
 // per-CTA copy at the start of the kernel's dynamic shared memory -- (cosh(m d), sinh(m d))
-// for m < 4096, 64 KB, read without a branch.  exp_scale_fill() copies only the rows the
-// launch can reach (m <= kh_max / d + 1, kh_max = max k h over the call's rows and layers,
-// which the range guard S9 bounds by 350).  Lanes of a warp hold neighbouring velocities, so
-// their m mostly coincide (broadcast reads).
+// for m < 5680 (d = 1/16: th < 354.97), 89 KB, read without a branch.  exp_scale_fill()
+// copies only the rows the launch can reach (m <= kh_max / d + 1, kh_max = max k h over the
+// call's rows and layers).  Lanes of a warp hold neighbouring velocities, so their m mostly
+// coincide (broadcast reads).
 constexpr unsigned kExpTabBytes = kExpTabN * 16u;
 
 __device__ __forceinline__ int exp_rows_needed(double kh_max)
@@ -156,6 +154,16 @@ __device__ __forceinline__ void sts_s32(unsigned a, int v)
 {
     asm volatile("st.shared.s32 [%0], %1;" : : "r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ int lds_s8(unsigned a)
+{
+    int v;
+    asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_s8(unsigned a, int v)
+{
+    asm volatile("st.shared.s8 [%0], %1;" : : "r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ LayerConst load_lc_at(unsigned a)
 {
     const double2 p = lds_v2(a), q = lds_v2(a + 16), r = lds_v2(a + 32);
@@ -190,7 +198,7 @@ __device__ __forceinline__ double rsqrt_fast(double q)
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
     const double e = fma(-q * y, y, 1.0);
-    return fma(y * e, fma(e, c_k[5], 0.5), y);
+    return fma(y * e, fma(e, c_k[3], 0.5), y);
 }
 
 // sqrt(q) and 1/sqrt(q) for finite q > 0: x = q * (1/sqrt q) (~1.5 ulp).  No residual
@@ -203,29 +211,28 @@ __device__ __forceinline__ void sqrt_rsqrt(double q, double &x, double &rx)
 }
 
 // cosh and sinh of th in [0, 350] (the range guard S9 bounds k h_e by 350 and x <= 1).
-// th = m d + r with d = ln2/8, |r| <= ln2/16; with A = cosh(m d), B = sinh(m d) from the
-// table and E = cosh r - 1, O = sinh r (near-minimax degree-3 polynomials in r^2, rel. err
-// < 6e-19):
+// th = m d + r with d = 1/16 (m = round(16 th); r = th - m/16 is exact), |r| <= 1/32; with
+// A = cosh(m d), B = sinh(m d) from the table and E = cosh r - 1, O = sinh r (near-minimax
+// polynomials in r^2: degree 2 for E / r^2, abs. err of E < 8e-19; degree 3 for O / r, rel.
+// err < 5e-20):
 //   cosh th = A (1 + E) + B O,   sinh th = B (1 + E) + A O.
 // At m = 0 (A = 1, B = 0) sinh th = O exactly structured (no cancellation at small th); for
-// m >= 1, B and A O do not cancel (th >= m d / 2).
+// m >= 1, B and A O do not cancel (th >= m d / 2).  15 FP64 operations, no branch (the
+// table covers th < 354.97; the index is clamped so a NaN argument stays in bounds).
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, unsigned tab)
 {
-    const double t = fma(th, c_k[0], kShifter);
+    const double t = fma(th, kExpInvD, kShifter);
     const double md = t - kShifter;
-    const unsigned m = (unsigned)__double2loint(t);
-    double r = fma(md, -kExpD_hi, th);                     // exact (m kExpD_hi has <= 33 bits)
-    r = fma(md, -c_k[1], r);
+    const unsigned m = min((unsigned)__double2loint(t), (unsigned)(kExpTabN - 1));
+    const double r = fma(md, -kExpD, th);                  // exact
     const double u = r * r;
-    double pe = fma(kExpE3_0, u, c_expE3[1]);              // E / r^2
+    double pe = fma(kExpE2_0, u, c_expE2[1]);              // E / r^2
     double po = fma(kExpO3_0, u, c_expO3[1]);              // O / r
+    pe = fma(pe, u, c_expE2[2]);
 #pragma unroll
-    for (int i = 2; i < 4; ++i) {
-        pe = fma(pe, u, c_expE3[i]);
-        po = fma(po, u, c_expO3[i]);
-    }
+    for (int i = 2; i < 4; ++i) po = fma(po, u, c_expO3[i]);
     const double E = pe * u, O = po * r;
-    const double2 ab = lds_v2(tab + (m & (unsigned)(kExpTabN - 1)) * 16u);
+    const double2 ab = lds_v2(tab + m * 16u);
     const double A = ab.x, B = ab.y;
     ch = fma(A, E, fma(B, O, A));
     sh = fma(B, E, fma(A, O, B));
@@ -248,12 +255,12 @@ __device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, dou
 
 __device__ __forceinline__ void sin_cos(double th, double &sn, double &cs)
 {
-    const double t = fma(th, c_k[2], kShifter);
+    const double t = fma(th, c_k[0], kShifter);
     const double nd = t - kShifter;
     const int n = __double2loint(t);
     double r = fma(nd, -kPio2Hi, th);          // exact (n * kPio2Hi has <= 40 bits)
-    r = fma(nd, -c_k[3], r);
-    r = fma(nd, -c_k[4], r);
+    r = fma(nd, -c_k[1], r);
+    r = fma(nd, -c_k[2], r);
     sin_cos_reduced(r, n, sn, cs);
 }
 

@@ -19,6 +19,7 @@
 // the load imbalance the paper repartitions for.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cmath>
@@ -455,11 +456,13 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 #define MASW_MODELS_UNROLL 1
 #endif
 constexpr int kModelRows = 64;
-// ONE CTA per SM: one copy of the 64 KB cosh/sinh table serves all of its warps.
+// ONE CTA per SM: one copy of the 89 KB cosh/sinh table serves all of its warps; as many
+// warps as the per-warp caches leave room for, up to kModelsBlock / 32 (16 for N <= 6).
 #ifndef MASW_MODELS_BLOCK
 #define MASW_MODELS_BLOCK 512
 #endif
 constexpr int kModelsBlock = MASW_MODELS_BLOCK;
+constexpr int kModelsMinWarps = 12;
 
 // Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
 // velocities (S4), k per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
@@ -471,7 +474,7 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
     return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
                    2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
                    (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
-                   (unsigned)kModelRows * 4u +                             // carried sign per row
+                   (unsigned)kModelRows +                                  // carried sign per row (s8)
                    32u * lane_cache_stride(N));                            // per-lane roots
 }
 
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
     double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
     double *kr = vel + 2 * (N + 1);
-    int *carry = reinterpret_cast<int *>(kr + kModelRows);              // per row: last sign
+    signed char *carry = reinterpret_cast<signed char *>(kr + kModelRows);   // per row: last sign
     const unsigned stride = lane_cache_stride(N);
     unsigned char *cl = reinterpret_cast<unsigned char *>(carry + kModelRows) + (unsigned)lane * stride;
 
@@ -620,7 +623,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                 // first-sign-change bookkeeping of row r for this chunk (lane signs s, bad)
                 auto settle = [&](int r, int s, bool bad) {
                     int sprev = __shfl_up_sync(FULL, s, 1);
-                    if (lane == 0) sprev = lds_s32(ya + 4u * (unsigned)r);
+                    if (lane == 0) sprev = lds_s8(ya + (unsigned)r);
                     const bool ev = valid && (bad || (j > 0 && s != sprev));
                     const unsigned mask = __ballot_sync(FULL, ev);
                     if (mask) {
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                         team_alg += (unsigned long long)(first + 1);
                         found |= 1u << (r - half * 32);
                     } else if (lane == 31) {
-                        sts_s32(ya + 4u * (unsigned)r, s);   // carried to the next chunk
+                        sts_s8(ya + (unsigned)r, s);   // carried to the next chunk
                     }
                 };
                 auto hs_of = [&](double k) {
@@ -764,7 +767,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
         __syncwarp();   // the next item rewrites this warp's constants
     }
     if (a.team_dets && lane == 0)
-        a.team_dets[(long long)blockIdx.x * (kModelsBlock / 32) + warp] = team_alg;
+        a.team_dets[(long long)blockIdx.x * (blockDim.x / 32) + warp] = team_alg;
 
     my_alg = warp_sum_u64(my_alg);
     my_eval = warp_sum_u64(my_eval);
@@ -926,19 +929,28 @@ long long scan_teams(const ScanArgs &a, int team_warps, int device)
     return t;
 }
 
-// Model-major launch: one work item per (model, block of kModelRows wavelengths).
-static size_t models_smem(int N)
+// Model-major launch: one work item per (model, block of kModelRows wavelengths); one CTA per
+// SM with as many warps as fit beside the table (up to kModelsBlock / 32, at least
+// kModelsMinWarps; 0 = the caches do not fit).
+static int models_warps(int N, int device)
 {
-    return kExpTabBytes + (size_t)(kModelsBlock / 32) * (size_t)warp_model_bytes(N);
+    const size_t static_smem = 16;
+    const size_t optin = smem_optin_limit(device);
+    if (optin < kExpTabBytes + static_smem) return 0;
+    const size_t w = (optin - kExpTabBytes - static_smem) / (size_t)warp_model_bytes(N);
+    const int warps = (int)std::min<size_t>(w, (size_t)(kModelsBlock / 32));
+    return warps >= kModelsMinWarps ? warps : 0;
 }
 
 static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
                                  long long *warps_out, bool dry, int *per_sm_out = nullptr)
 {
-    const size_t smem = models_smem(a.mod.N);
+    const int wpc = models_warps(a.mod.N, device);
+    const size_t smem = kExpTabBytes + (size_t)wpc * (size_t)warp_model_bytes(a.mod.N);
     auto kern = scan_models_kernel;
     const int sms = sm_count(device);
-    const long long key = ((long long)device << 48) | (1ll << 47) | (long long)smem;
+    const long long key = ((long long)device << 48) | (1ll << 47) | ((long long)wpc << 32) |
+                          (long long)smem;
     int per_sm = 0;
     {
         std::lock_guard<std::mutex> g(g_cache_mu);
@@ -948,14 +960,13 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
     if (per_sm == 0) {
         // a cache that does not fit is "0 CTAs per SM", not an error (and must not leave a
         // pending runtime error for the next launch's cudaGetLastError)
-        const size_t static_smem = 16;
-        if (smem + static_smem > smem_optin_limit(device)) {
+        if (wpc == 0) {
             per_sm = -1;
         } else {
             if (ensure_smem_optin(kern, device, 1) != cudaSuccess) {
                 cudaGetLastError();
                 per_sm = -1;
-            } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kModelsBlock,
+            } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc,
                                                                      smem) != cudaSuccess) {
                 cudaGetLastError();
                 per_sm = -1;
@@ -970,12 +981,12 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
     if (per_sm == 0) return cudaErrorInvalidConfiguration;
     const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
     int64_t blocks = (int64_t)sms * per_sm;
-    const int64_t need = (items + kModelsBlock / 32 - 1) / (kModelsBlock / 32);
+    const int64_t need = (items + wpc - 1) / wpc;
     if (need < blocks) blocks = need;
     if (blocks < 1) blocks = 1;
-    if (warps_out) *warps_out = blocks * (kModelsBlock / 32);
+    if (warps_out) *warps_out = blocks * wpc;
     if (dry) return cudaSuccess;
-    kern<<<(unsigned)blocks, kModelsBlock, smem, st>>>(a);
+    kern<<<(unsigned)blocks, 32 * wpc, smem, st>>>(a);
     count_launch();
     return cudaGetLastError();
 }
@@ -983,8 +994,9 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
 bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
 {
     // unless forced: enough work items to fill the GPU several times over and several
-    // wavelengths per model to share the cache; and one 16-warp CTA per SM with the table
-    // and the per-warp caches must fit (N <= 7)
+    // wavelengths per model to share the cache; and one CTA per SM of >= kModelsMinWarps
+    // warps with the table and the per-warp caches must fit (16 warps for N <= 6, 14 for
+    // N = 7, 13 for N = 8)
     const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
     const int sms = sm_count(device);
     if (a.sched != 0) return false;

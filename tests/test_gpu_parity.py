@@ -72,6 +72,29 @@ def test_det_grid_parity_uniform_n10(masw, orc):
     assert float(np.nanmax(rel[dom])) <= parity.DET_RTOL
 
 
+def test_det_grid_parity_thick_layers_whole_exp_range(masw, orc):
+    """k h_e up to 349.7 (just inside the S9 guard): the cosh/sinh table is read at every m up
+    to its last rows (th = k h x from ~0 to 349.7), including the previously out-of-table range
+    th > 256.  Det parity with the oracle in the S15 domain, and the guard at 350."""
+    h = np.array([0.7, 9.0, 55.65])
+    beta = np.array([150.0, 220.0, 300.0, 400.0])
+    alpha = np.array([600.0, 800.0, 1000.0, 1440.0])
+    rho = np.array([1800.0, 1850.0, 1900.0, 2000.0])
+    lam = np.array([1.0, 1.4, 2.5, 7.0])                 # k h_2 = 349.7, 249.8, 139.9, 50.0
+    c = np.linspace(76.0, 600.0, 131)
+    gre, gim, gex = masw.masw_det_grid(h, alpha, beta, rho, lam, c)
+    st, omant, oex, _ = orc.det_grid(h, alpha, beta, rho, lam, c)
+    assert st == 0
+    kap = orc.det_grid_kappa(h, alpha, beta, rho, lam, c)
+    rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
+    dom = parity.det_domain(omant, oex, c, beta.min(), kap)
+    assert dom.mean() > 0.5
+    assert float(np.nanmax(rel[dom])) <= parity.DET_RTOL
+    with pytest.raises(masw.MaswError) as e:
+        masw.masw_det_grid(np.array([0.7, 9.0, 55.8]), alpha, beta, rho, lam, c)
+    assert e.value.code == masw.E_RANGE
+
+
 @pytest.mark.parametrize("seed", [0, 1])
 def test_det_parity_random_ensemble_points(masw, orc, seed):
     """Det parity on random C5 models at random (lambda, c): 16 models x 40 lambda x 96 c."""
