@@ -243,6 +243,15 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, uns
 // polynomials on |r| <= pi/4: sin to r^13, cos to r^14).  No branches; the caller
 // routes larger arguments to sin_cos_large.
 constexpr double kTrigMax = 8.0e5;
+
+// Sign / range tests on the high word in the integer pipe (a DSETP occupies the FP64 pipe):
+// is_pos(x) == (x > 0) for every x the scans test (nonzero by S4, or NaN -> either branch
+// gives NaN); trig_fast(th) == (th < 2^19) for th >= 0 (NaN -> the large-argument path).
+__device__ __forceinline__ bool is_pos(double x) { return __double2hiint(x) > 0; }
+__device__ __forceinline__ bool trig_fast(double th)
+{
+    return (unsigned)__double2hiint(th) < 0x41200000u;   // 2^19 < kTrigMax
+}
 // pi/2 in five parts, the first four of <= 23 significant bits: n * part is exact for
 // n < 2^30, so the large-argument reduction below is accurate for th < 2^30 * pi/2.
 constexpr double kPio2L_1 = 1.570796251296997;
@@ -324,7 +333,7 @@ __device__ __forceinline__ void wave_trig(double q, double kh, double &C, double
     sqrt_rsqrt(-q, xi, rq);
     const double th = kh * xi;
     double sn, cs;
-    if (th < kTrigMax) {
+    if (trig_fast(th)) {
         sin_cos(th, sn, cs);
     } else {
         sin_cos_large(th, sn, cs);
@@ -407,8 +416,8 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
     double Cr, XSr, SXr, Cs, XSs, SXs;
     // The P wave is hyperbolic unless c exceeds alpha (rare); each S-wave branch carries its
     // own branch-free copy of the P wave so the two independent chains interleave (ILP).
-    if (qa > 0.0) {
-        if (qb > 0.0) {
+    if (is_pos(qa)) {
+        if (is_pos(qb)) {
             wave_hyp(qa, L.kh, Cr, XSr, SXr, tab);
             wave_hyp(qb, L.kh, Cs, XSs, SXs, tab);
         } else {
@@ -564,7 +573,7 @@ __device__ __forceinline__ void wave_trig_root(double xneg, double rx, double kh
     const double xi = -xneg;
     const double th = kh * xi;
     double sn, cs;
-    if (th < kTrigMax) {
+    if (trig_fast(th)) {
         sin_cos(th, sn, cs);
     } else {
         sin_cos_large(th, sn, cs);
@@ -584,8 +593,8 @@ __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, d
 {
     const double kh = k * M.kh;
     double Cr, XSr, SXr, Cs, XSs, SXs;
-    if (a.x > 0.0) {
-        if (b.x > 0.0) {
+    if (is_pos(a.x)) {
+        if (is_pos(b.x)) {
             wave_hyp_root(a.x, a.y, kh, Cr, XSr, SXr, tab);
             wave_hyp_root(b.x, b.y, kh, Cs, XSs, SXs, tab);
         } else {
@@ -611,8 +620,8 @@ __device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka,
     const double kha = ka * M.kh, khb = kb * M.kh;
     double Cra, XSra, SXra, Csa, XSsa, SXsa;
     double Crb, XSrb, SXrb, Csb, XSsb, SXsb;
-    if (a.x > 0.0) {
-        if (b.x > 0.0) {
+    if (is_pos(a.x)) {
+        if (is_pos(b.x)) {
             wave_hyp_root(a.x, a.y, kha, Cra, XSra, SXra, tab);
             wave_hyp_root(a.x, a.y, khb, Crb, XSrb, SXrb, tab);
             wave_hyp_root(b.x, b.y, kha, Csa, XSsa, SXsa, tab);
@@ -1140,8 +1149,10 @@ struct BlockSign {
         SignOut o;
         o.ok = (worst <= kBlockMultExp) && (dmin > 0) && (dmax < 0x7ff) && (exp_of(dre) < 0x7ff);
         o.bad = false;
-        const bool neg = ((sgn >> 31) != 0) ^ (dre < 0.0);
-        o.sign = (dre == 0.0) ? 0 : (neg ? -1 : 1);
+        const int hi = __double2hiint(dre);
+        const bool neg = ((sgn >> 31) != 0) ^ (hi < 0);
+        const bool zero = ((hi & 0x7fffffff) | __double2loint(dre)) == 0;
+        o.sign = zero ? 0 : (neg ? -1 : 1);
         return o;
     }
 };
