@@ -42,17 +42,20 @@ constexpr double kMaxKH = 350.0;               // reading S9 range guard
 constexpr double kPerturbTol = 1e-4;           // reading S4
 constexpr double kPerturbFactor = 1.0 - 1e-4;  // reading S4
 
-// Per-row constants of one finite layer e (index N holds the half-space's ia2, ib2, mu).
-// 48 bytes, 16-byte aligned: read from shared memory as three 128-bit loads.
+// Per-row constants of one finite layer e (index N holds the half-space's ia2, ib2, krho,
+// b2).  48 bytes, 16-byte aligned: read from shared memory as three 128-bit loads.
 struct __align__(16) LayerConst {
     double kh;    // k * h_e
     double ia2;   // 1 / alpha_e^2
     double ib2;   // 1 / beta_e^2
     double krho;  // k * rho_e
-    double mu;    // k * rho_e * beta_e^2
-    double pad;
+    double b2;    // 2 beta_e^2  (mu = k rho_e beta_e^2 = krho * (b2 / 2), exactly: lc_mu)
+    double aux;   // scans only (else 0): e < N: rho_e / rho_(e+1); e = N: rho_N beta_N^2 / rho_(N-1)
 };
 static_assert(sizeof(LayerConst) == 48, "LayerConst layout");
+
+// mu = (k) rho beta^2, bitwise equal to krho * (beta * beta): b2 / 2 = beta^2 exactly
+__device__ __forceinline__ double lc_mu(const LayerConst &L) { return L.krho * (0.5 * L.b2); }
 
 __device__ __forceinline__ LayerConst load_lc(const LayerConst *p)
 {
@@ -63,8 +66,8 @@ __device__ __forceinline__ LayerConst load_lc(const LayerConst *p)
     L.ia2 = a.y;
     L.ib2 = b.x;
     L.krho = b.y;
-    L.mu = c.x;
-    L.pad = c.y;
+    L.b2 = c.x;
+    L.aux = c.y;
     return L;
 }
 
@@ -172,8 +175,8 @@ __device__ __forceinline__ LayerConst load_lc_at(unsigned a)
     L.ia2 = p.y;
     L.ib2 = q.x;
     L.krho = q.y;
-    L.mu = r.x;
-    L.pad = r.y;
+    L.b2 = r.x;
+    L.aux = r.y;
     return L;
 }
 
@@ -399,6 +402,38 @@ __device__ __forceinline__ Elem elem_from_triples(double Cr, double XSr, double 
     return E;
 }
 
+// The same element without its scalar factor, for the sign scan: E = f U with f = k rho c^2 / D
+// and, since mu (1 + s^2) = k rho (2 beta^2 - c^2) = f D (2 beta^2 / c^2 - 1),
+//   U = the element's brackets, with k12's  g12 = Cr Cs - XSr XSs - 1 + kappa D,
+//   kappa = 1 - 2 beta^2 / c^2  (per layer and velocity; from b2 = 2 beta^2 and 1/c^2).
+// No reciprocal and no scaling products: det_sign_block_u carries f through the recursion
+// as ratios f_e / f_(e+1) = (rho_e / rho_(e+1)) D_(e+1) / D_e (rr = rho_e / rho_(e+1)).
+struct ElemU {
+    double g11, g12, g13, g14, g22, g24, D, rr;
+};
+
+__device__ __forceinline__ ElemU elemu_from_triples(double Cr, double XSr, double SXr, double Cs,
+                                                    double XSs, double SXs, double kap, double rr)
+{
+    const double cm1 = fma(Cr, Cs, -1.0);                              // Cr Cs - 1
+    ElemU U;
+    U.D = fma(XSr, XSs, fma(-2.0, cm1, SXr * SXs));
+    U.g11 = fma(Cr, SXs, -XSr * Cs);
+    U.g12 = fma(kap, U.D, fma(-XSr, XSs, cm1));
+    U.g13 = XSr - SXs;
+    U.g14 = Cs - Cr;
+    U.g22 = fma(SXr, Cs, -Cr * XSs);
+    U.g24 = XSs - SXr;
+    U.rr = rr;
+    return U;
+}
+
+// kappa_e = 1 - 2 beta_e^2 / c^2
+__device__ __forceinline__ double lc_kappa(const LayerConst &L, double ic2)
+{
+    return fma(-L.b2, ic2, 1.0);
+}
+
 // Rare case c > alpha_e (both waves possibly trigonometric): kept out of line so the hot
 // loop's code stays small (instruction-cache pressure was measured: no_instruction stalls).
 static __device__ __noinline__ void waves_general(double qa, double qb, double kh, double *t,
@@ -430,7 +465,31 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
         Cr = t[0]; XSr = t[1]; SXr = t[2];
         Cs = t[3]; XSs = t[4]; SXs = t[5];
     }
-    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, L.mu, c2);
+    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, L.krho, lc_mu(L), c2);
+}
+
+// layer_elem without the factor f (ElemU; ic2 = 1/c^2 of the same c2).
+__device__ __forceinline__ ElemU layer_elem_u(const LayerConst &L, double c2, double ic2,
+                                              unsigned tab)
+{
+    const double qa = fma(-c2, L.ia2, 1.0);   // r^2
+    const double qb = fma(-c2, L.ib2, 1.0);   // s^2
+    double Cr, XSr, SXr, Cs, XSs, SXs;
+    if (is_pos(qa)) {
+        if (is_pos(qb)) {
+            wave_hyp(qa, L.kh, Cr, XSr, SXr, tab);
+            wave_hyp(qb, L.kh, Cs, XSs, SXs, tab);
+        } else {
+            wave_hyp(qa, L.kh, Cr, XSr, SXr, tab);
+            wave_trig(qb, L.kh, Cs, XSs, SXs);
+        }
+    } else {
+        double t[6];
+        waves_general(qa, qb, L.kh, t, tab);
+        Cr = t[0]; XSr = t[1]; SXr = t[2];
+        Cs = t[3]; XSs = t[4]; SXs = t[5];
+    }
+    return elemu_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, lc_kappa(L, ic2), L.aux);
 }
 
 // -------------------------------------------------------------- stable element (f3)
@@ -534,11 +593,11 @@ __device__ __forceinline__ Elem elem_stable_ht(double kh, double c2, double ia2,
 __device__ __forceinline__ Elem layer_elem_stable(const LayerConst &L, double c2, unsigned tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0), qb = fma(-c2, L.ib2, 1.0);
-    if (qa > 0.0 && qb > 0.0) return elem_stable_hh(L.kh, c2, L.ia2, L.ib2, L.krho, L.mu, tab);
-    if (qa > 0.0) return elem_stable_ht(L.kh, c2, L.ia2, L.ib2, L.krho, L.mu, tab);
+    if (qa > 0.0 && qb > 0.0) return elem_stable_hh(L.kh, c2, L.ia2, L.ib2, L.krho, lc_mu(L), tab);
+    if (qa > 0.0) return elem_stable_ht(L.kh, c2, L.ia2, L.ib2, L.krho, lc_mu(L), tab);
     double t[6];   // both trigonometric: bounded functions, the direct formulas
     waves_general(qa, qb, L.kh, t, tab);
-    return elem_from_triples(t[0], t[1], t[2], t[3], t[4], t[5], L.krho, L.mu, c2);
+    return elem_from_triples(t[0], t[1], t[2], t[3], t[4], t[5], L.krho, lc_mu(L), c2);
 }
 
 // -------------------------------------------------------------- wavelength-free terms
@@ -584,7 +643,7 @@ __device__ __forceinline__ void wave_trig_root(double xneg, double rx, double kh
 }
 
 // Element of K / k for layer M at wavenumber k from the cached roots a (P wave) and b (S wave).
-// M holds the model's k-free constants: M.kh = h, M.krho = rho, M.mu = rho beta^2; only
+// M holds the model's k-free constants: M.kh = h, M.krho = rho, M.b2 = 2 beta^2; only
 // k h = k * M.kh depends on the wavelength (formed exactly as the row scan's LayerConst
 // fill forms it, so both scans compute bitwise-identical elements).
 __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, double2 a,
@@ -607,7 +666,7 @@ __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, d
         Cr = t[0]; XSr = t[1]; SXr = t[2];
         Cs = t[3]; XSs = t[4]; SXs = t[5];
     }
-    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, M.krho, M.mu, c2);
+    return elem_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, M.krho, lc_mu(M), c2);
 }
 
 // Elements of layer M for two wavenumbers ka, kb (two wavelengths of one model) at the same
@@ -642,8 +701,66 @@ __device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka,
         Crb = t[0]; XSrb = t[1]; SXrb = t[2];
         Csb = t[3]; XSsb = t[4]; SXsb = t[5];
     }
-    Ea = elem_from_triples(Cra, XSra, SXra, Csa, XSsa, SXsa, M.krho, M.mu, c2);
-    Eb = elem_from_triples(Crb, XSrb, SXrb, Csb, XSsb, SXsb, M.krho, M.mu, c2);
+    Ea = elem_from_triples(Cra, XSra, SXra, Csa, XSsa, SXsa, M.krho, lc_mu(M), c2);
+    Eb = elem_from_triples(Crb, XSrb, SXrb, Csb, XSsb, SXsb, M.krho, lc_mu(M), c2);
+}
+
+// layer_elem_root / layer_elem_root2 without the factor f (ElemU), for the sign scans.
+__device__ __forceinline__ ElemU layer_elem_root_u(const LayerConst &M, double k, double2 a,
+                                                   double2 b, double c2, double ic2,
+                                                   unsigned tab)
+{
+    const double kh = k * M.kh;
+    double Cr, XSr, SXr, Cs, XSs, SXs;
+    if (is_pos(a.x)) {
+        if (is_pos(b.x)) {
+            wave_hyp_root(a.x, a.y, kh, Cr, XSr, SXr, tab);
+            wave_hyp_root(b.x, b.y, kh, Cs, XSs, SXs, tab);
+        } else {
+            wave_hyp_root(a.x, a.y, kh, Cr, XSr, SXr, tab);
+            wave_trig_root(b.x, b.y, kh, Cs, XSs, SXs);
+        }
+    } else {
+        double t[6];
+        waves_general(fma(-c2, M.ia2, 1.0), fma(-c2, M.ib2, 1.0), kh, t, tab);
+        Cr = t[0]; XSr = t[1]; SXr = t[2];
+        Cs = t[3]; XSs = t[4]; SXs = t[5];
+    }
+    return elemu_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, lc_kappa(M, ic2), M.aux);
+}
+
+__device__ __forceinline__ void layer_elem_root2_u(const LayerConst &M, double ka, double kb,
+                                                   double2 a, double2 b, double c2, double ic2,
+                                                   unsigned tab, ElemU &Ea, ElemU &Eb)
+{
+    const double kha = ka * M.kh, khb = kb * M.kh;
+    double Cra, XSra, SXra, Csa, XSsa, SXsa;
+    double Crb, XSrb, SXrb, Csb, XSsb, SXsb;
+    if (is_pos(a.x)) {
+        if (is_pos(b.x)) {
+            wave_hyp_root(a.x, a.y, kha, Cra, XSra, SXra, tab);
+            wave_hyp_root(a.x, a.y, khb, Crb, XSrb, SXrb, tab);
+            wave_hyp_root(b.x, b.y, kha, Csa, XSsa, SXsa, tab);
+            wave_hyp_root(b.x, b.y, khb, Csb, XSsb, SXsb, tab);
+        } else {
+            wave_hyp_root(a.x, a.y, kha, Cra, XSra, SXra, tab);
+            wave_hyp_root(a.x, a.y, khb, Crb, XSrb, SXrb, tab);
+            wave_trig_root(b.x, b.y, kha, Csa, XSsa, SXsa);
+            wave_trig_root(b.x, b.y, khb, Csb, XSsb, SXsb);
+        }
+    } else {
+        double t[6];
+        const double qa = fma(-c2, M.ia2, 1.0), qb = fma(-c2, M.ib2, 1.0);
+        waves_general(qa, qb, kha, t, tab);
+        Cra = t[0]; XSra = t[1]; SXra = t[2];
+        Csa = t[3]; XSsa = t[4]; SXsa = t[5];
+        waves_general(qa, qb, khb, t, tab);
+        Crb = t[0]; XSrb = t[1]; SXrb = t[2];
+        Csb = t[3]; XSsb = t[4]; SXsb = t[5];
+    }
+    const double kap = lc_kappa(M, ic2);
+    Ea = elemu_from_triples(Cra, XSra, SXra, Csa, XSsa, SXsa, kap, M.aux);
+    Eb = elemu_from_triples(Crb, XSrb, SXrb, Csb, XSsb, SXsb, kap, M.aux);
 }
 
 // Half-space element K_hs = mu [[r w/(1-rs), w/(1-rs) - 2], [., s w/(1-rs)]], w = 1 - s^2 =
@@ -1157,6 +1274,135 @@ struct BlockSign {
     }
 };
 
+// The same recursion on the f-free elements (ElemU, E_e = f_e U_e): with S_t = f_t S^_t
+// (node t's leading block over its lower layer's factor; det S_t = f_t^2 det S^_t has the
+// sign of det S^_t, and the multipliers S_t^-1 B_t = S^_t^-1 G_t are unchanged),
+//   S^_0 = top(U_0),
+//   S^_(t+1) = (f_t / f_(t+1)) X_t / d_t + top(U_(t+1)),  X_t = d_t bot(U_t) - G_t^T adj(S^_t) G_t,
+//   d_t = det S^_t,   f_t / f_(t+1) = rr_t D_(t+1) / D_t,
+// i.e. one reciprocal of p_t = D_t d_t per node and none per element; the last node
+// S_N = f_(N-1) X / d + K_hs is scaled by the real d / f_(N-1):  Z = X + p K_hs / (rho_(N-1) c^2)
+// (same sign of Re det).  The half-space is passed pre-scaled (halfspace_k with
+// mu' = rho_N beta_N^2 / (rho_(N-1) c^2)).  p_t is also certified (nonzero, finite: D_t = 0 is
+// a pole of the element, which the GEPP re-evaluation reports as non-finite).
+struct BlockSignU {
+    ElemU P;                // the previous layer's element
+    double s11, s12, s22;   // S^_t
+    unsigned sgn;
+    int worst, dmin, dmax;  // as BlockSign (dmin / dmax over p_t)
+    double x11, x12, x22, rg;
+
+    __device__ __forceinline__ void init(const ElemU &E)
+    {
+        P = E;
+        s11 = E.g11;
+        s12 = E.g12;
+        s22 = E.g22;
+        sgn = 0u;
+        worst = -4096;
+        dmin = 0x7ff;
+        dmax = 0;
+    }
+
+    // X = d bot(P) - G^T adj(S^) G, p = D_P d
+    __device__ __forceinline__ double eliminate()
+    {
+        const double b11 = P.g13, b12 = P.g14, b22 = P.g24;
+        const double d = fma(s11, s22, -(s12 * s12));
+        const double w11 = fma(s22, b11, s12 * b12);
+        const double w12 = fma(s22, b12, -s12 * b22);
+        const double w21 = fma(-s12, b11, -s11 * b12);
+        const double w22 = fma(-s12, b12, s11 * b22);
+        const double m11 = fma(b11, w11, -b12 * w21);
+        const double m12 = fma(b11, w12, -b12 * w22);
+        const double m22 = fma(b12, w12, b22 * w22);
+        x11 = fma(P.g11, d, -m11);
+        x12 = fma(-P.g12, d, -m12);
+        x22 = fma(P.g22, d, -m22);
+        const double p = P.D * d;
+        sgn ^= (unsigned)__double2hiint(d);
+        const int ed = exp_of(d), ep = exp_of(p);
+        const int ew = max(max(exp_of(w11), exp_of(w12)), max(exp_of(w21), exp_of(w22)));
+        worst = max(worst, ew - ed);
+        dmin = min(dmin, ep);
+        dmax = max(dmax, ep);
+        return p;
+    }
+    __device__ __forceinline__ void pre() { rg = P.rr * rcp_fast(eliminate()); }
+    __device__ __forceinline__ void post(const ElemU &Q)
+    {
+        const double g = rg * Q.D;
+        s11 = fma(g, x11, Q.g11);
+        s12 = fma(g, x12, Q.g12);
+        s22 = fma(g, x22, Q.g22);
+        P = Q;
+    }
+
+    // H: K_hs scaled by 1 / (rho_(N-1) c^2)
+    __device__ __forceinline__ SignOut finish(const HalfSpace &H)
+    {
+        const double p = eliminate();
+        const double z11 = fma(p, H.h11r, x11), z12 = fma(p, H.h12r, x12),
+                     z22 = fma(p, H.h22r, x22);
+        double dre;
+        if (H.real) {
+            dre = fma(z11, z22, -(z12 * z12));
+        } else {
+            const double i11 = p * H.h11i, i12 = p * H.h12i, i22 = p * H.h22i;
+            dre = fma(z11, z22, -i11 * i22) - fma(z12, z12, -i12 * i12);
+        }
+        SignOut o;
+        o.ok = (worst <= kBlockMultExp) && (dmin > 0) && (dmax < 0x7ff) && (exp_of(dre) < 0x7ff);
+        o.bad = false;
+        const int hi = __double2hiint(dre);
+        const bool neg = ((sgn >> 31) != 0) ^ (hi < 0);
+        const bool zero = ((hi & 0x7fffffff) | __double2loint(dre)) == 0;
+        o.sign = zero ? 0 : (neg ? -1 : 1);
+        return o;
+    }
+};
+
+template <int UNROLL, class ElemFn, class HsFn>
+__device__ __forceinline__ SignOut det_sign_block_u(int N, ElemFn &&elem, HsFn &&hs)
+{
+    BlockSignU st;
+    st.init(elem(0));
+    constexpr int kU = UNROLL;
+#pragma unroll kU
+    for (int t = 0; t + 1 < N; ++t) {
+        st.pre();
+        st.post(elem(t + 1));
+    }
+    return st.finish(hs());
+}
+
+template <int UNROLL, class Elem2Fn, class Hs2Fn>
+__device__ __forceinline__ void det_sign_block_u_pair(int N, Elem2Fn &&elem2, Hs2Fn &&hs2,
+                                                      SignOut &oa, SignOut &ob)
+{
+    BlockSignU A, B;
+    {
+        ElemU ea, eb;
+        elem2(0, ea, eb);
+        A.init(ea);
+        B.init(eb);
+    }
+    constexpr int kU = UNROLL;
+#pragma unroll kU
+    for (int t = 0; t + 1 < N; ++t) {
+        A.pre();
+        B.pre();
+        ElemU qa, qb;
+        elem2(t + 1, qa, qb);
+        A.post(qa);
+        B.post(qb);
+    }
+    HalfSpace ha, hb;
+    hs2(ha, hb);
+    oa = A.finish(ha);
+    ob = B.finish(hb);
+}
+
 template <int UNROLL, class ElemFn, class HsFn>
 __device__ __forceinline__ SignOut det_sign_block(int N, ElemFn &&elem, HsFn &&hs)
 {
@@ -1222,7 +1468,7 @@ __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
         },
         [&] {
             const LayerConst H = load_lc(lc + N);
-            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.mu);
+            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
         });
 }
 

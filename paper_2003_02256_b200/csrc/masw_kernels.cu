@@ -299,8 +299,10 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             x.ia2 = 1.0 / (al * al);
             x.ib2 = 1.0 / (be * be);
             x.krho = rh;
-            x.mu = rh * (be * be);
-            x.pad = 0.0;
+            x.b2 = 2.0 * (be * be);
+            // f-free sign recursion (BlockSignU): rho_e / rho_(e+1); half-space: mu' factor
+            x.aux = (e < N) ? rh / a.mod.rho[m * (N + 1) + e + 1]
+                            : (rh * (be * be)) / a.mod.rho[m * (N + 1) + N - 1];
             lc[e] = x;
             vel[2 * e] = al;
             vel[2 * e + 1] = be;
@@ -343,17 +345,24 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
                 const double c2 = c * c;
                 SignOut so;
                 so.ok = false;
-                if (!a.pivoted)
-                    so = det_sign_block<MASW_LAYER_UNROLL>(
-                        N,
-                        [&](int e) {
-                            if constexpr (STABLE) return layer_elem_stable(load_lc(lc + e), c2, ta);
-                            else return layer_elem(load_lc(lc + e), c2, ta);
-                        },
-                        [&] {
-                            const LayerConst H = load_lc(lc + N);
-                            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.mu);
-                        });
+                if (!a.pivoted) {
+                    if constexpr (STABLE) {
+                        so = det_sign_block<MASW_LAYER_UNROLL>(
+                            N, [&](int e) { return layer_elem_stable(load_lc(lc + e), c2, ta); },
+                            [&] {
+                                const LayerConst H = load_lc(lc + N);
+                                return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
+                            });
+                    } else {
+                        const double ic2 = rcp_fast(c2);
+                        so = det_sign_block_u<MASW_LAYER_UNROLL>(
+                            N, [&](int e) { return layer_elem_u(load_lc(lc + e), c2, ic2, ta); },
+                            [&] {
+                                const LayerConst H = load_lc(lc + N);
+                                return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.aux * ic2);
+                            });
+                    }
+                }
                 if (so.ok) {
                     s = so.sign;
                 } else {
@@ -481,7 +490,7 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
 // GEPP sign for one lane of the model-major kernel (see row_det_gepp); the same element
 // and half-space evaluation as the kernel's hot path.
 static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, unsigned ha,
-                                                   unsigned hca, unsigned ta, double k,
+                                                   unsigned ta, double k,
                                                    double c2, int N)
 {
     const DetOut d = det_core<false, 0, 1>(
@@ -492,14 +501,8 @@ static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, uns
                                    lds_v2(ca + o + 16u), c2, ta);
         },
         [&] {
-            const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
-            HsRoot h;
-            h.r = rs.x;
-            h.s = rs.y;
-            h.gw = gt.x;
-            h.t = gt.y;
-            h.kase = lds_s32(hca + 32u);
-            return halfspace_k(h, lds_f64(ha + 32u));   // rho_N beta_N^2 (K / k)
+            const LayerConst H = load_lc_at(ha);   // as the row scan's GEPP forms it
+            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
         });
     return d.bad ? 2 : d.sign;
 }
@@ -560,8 +563,9 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             x.ia2 = 1.0 / (al * al);
             x.ib2 = 1.0 / (be * be);
             x.krho = rh;               // K / k: rho and rho beta^2 (see scan_kernel)
-            x.mu = rh * (be * be);
-            x.pad = 0.0;
+            x.b2 = 2.0 * (be * be);
+            x.aux = (e < N) ? rh / a.mod.rho[m * (N + 1) + e + 1]
+                            : (rh * (be * be)) / a.mod.rho[m * (N + 1) + N - 1];
             mc[e] = x;
             vel[2 * e] = al;
             vel[2 * e + 1] = be;
@@ -600,6 +604,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                 if (lane_near) c = perturb_velocity(vel, nv, c);
             }
             const double c2 = c * c;
+            const double ic2 = rcp_fast(c2);
             // wavelength-free terms of this lane's velocity (lane-private slots: no sync)
             {
                 double2 *rt = reinterpret_cast<double2 *>(cl);
@@ -608,11 +613,12 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                     rt[2 * e] = wave_root(fma(-c2, Lc.ia2, 1.0));
                     rt[2 * e + 1] = wave_root(fma(-c2, Lc.ib2, 1.0));
                 }
+                // the half-space element as BlockSignU takes it: K_hs / (rho_(N-1) c^2)
                 const LayerConst Hl = mc[N];
-                const HsRoot h = halfspace_root(Hl.ia2, Hl.ib2, c2);
-                rt[2 * N] = make_double2(h.r, h.s);
-                rt[2 * N + 1] = make_double2(h.gw, h.t);
-                *reinterpret_cast<int *>(rt + 2 * N + 2) = h.kase;
+                const HalfSpace H = halfspace_k(halfspace_root(Hl.ia2, Hl.ib2, c2), Hl.aux * ic2);
+                rt[2 * N] = make_double2(H.h11r, H.h12r);
+                rt[2 * N + 1] = make_double2(H.h22r, H.h11i);
+                rt[2 * N + 2] = make_double2(H.h12i, H.h22i);
             }
             const unsigned ca = opaque(smem_addr(cl));
             const unsigned hca = ca + 32u * (unsigned)N;
@@ -646,15 +652,21 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                         sts_s8(ya + (unsigned)r, s);   // carried to the next chunk
                     }
                 };
-                auto hs_of = [&](double k) {
-                    const double2 rs = lds_v2(hca), gt = lds_v2(hca + 16u);
-                            HsRoot h;
-                    h.r = rs.x;
-                    h.s = rs.y;
-                    h.gw = gt.x;
-                    h.t = gt.y;
-                    h.kase = lds_s32(hca + 32u);
-                    return halfspace_k(h, lds_f64(ha + 32u));   // rho_N beta_N^2 (K / k)
+                auto hs_scaled = [&] {   // K_hs / (rho_(N-1) c^2), k-free (cached above)
+                    const double2 p = lds_v2(hca), q = lds_v2(hca + 16u), r = lds_v2(hca + 32u);
+                    HalfSpace H;
+                    H.h11r = p.x;
+                    H.h12r = p.y;
+                    H.h22r = q.x;
+                    H.h11i = q.y;
+                    H.h12i = r.x;
+                    H.h22i = r.y;
+                    H.real = __double2hiint(H.h11i) == 0;   // +0 exactly below beta_N
+                    return H;
+                };
+                auto hs_gepp = [&] {     // K_hs / k, as the row scan's GEPP forms it
+                    const LayerConst H = load_lc_at(ha);
+                    return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
                 };
                 while (pend) {
                     const int r = half * 32 + __ffs(pend) - 1;
@@ -669,23 +681,23 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                         bool bad1 = false, bad2 = false;
                         if (valid) {
                             SignOut o1, o2;
-                            det_sign_block_pair<MASW_MODELS_UNROLL>(
+                            det_sign_block_u_pair<MASW_MODELS_UNROLL>(
                                 N,
-                                [&](int e, Elem &E1, Elem &E2) {
+                                [&](int e, ElemU &E1, ElemU &E2) {
                                     const unsigned o = 32u * (unsigned)e;
-                                    layer_elem_root2(load_lc_at(ma + 48u * (unsigned)e), k, k2,
-                                                     lds_v2(ca + o), lds_v2(ca + o + 16u), c2,
-                                                     ta, E1, E2);
+                                    layer_elem_root2_u(load_lc_at(ma + 48u * (unsigned)e), k, k2,
+                                                       lds_v2(ca + o), lds_v2(ca + o + 16u), c2,
+                                                       ic2, ta, E1, E2);
                                 },
                                 [&](HalfSpace &H1, HalfSpace &H2) {
-                                    H1 = hs_of(k);
-                                    H2 = hs_of(k2);
+                                    H1 = hs_scaled();
+                                    H2 = H1;
                                 },
                                 o1, o2);
                             if (o1.ok) {
                                 s1 = o1.sign;
                             } else {
-                                const int rr = models_det_gepp(ma, ca, ha, hca, ta, k, c2, N);
+                                const int rr = models_det_gepp(ma, ca, ha, ta, k, c2, N);
                                 bad1 = (rr == 2);
                                 s1 = bad1 ? 0 : rr;
                                 ++fb32;
@@ -693,7 +705,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                             if (o2.ok) {
                                 s2 = o2.sign;
                             } else {
-                                const int rr = models_det_gepp(ma, ca, ha, hca, ta, k2, c2, N);
+                                const int rr = models_det_gepp(ma, ca, ha, ta, k2, c2, N);
                                 bad2 = (rr == 2);
                                 s2 = bad2 ? 0 : rr;
                                 ++fb32;
@@ -712,19 +724,19 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                         SignOut so;
                         so.ok = false;
                         if (!a.pivoted)
-                            so = det_sign_block<MASW_MODELS_UNROLL>(
+                            so = det_sign_block_u<MASW_MODELS_UNROLL>(
                                 N,
                                 [&](int e) {
                                     const unsigned o = 32u * (unsigned)e;
-                                    return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
-                                                           lds_v2(ca + o), lds_v2(ca + o + 16u), c2,
-                                                           ta);
+                                    return layer_elem_root_u(load_lc_at(ma + 48u * (unsigned)e),
+                                                             k, lds_v2(ca + o),
+                                                             lds_v2(ca + o + 16u), c2, ic2, ta);
                                 },
-                                [&] { return hs_of(k); });
+                                hs_scaled);
                         if (so.ok) {
                             s = so.sign;
                         } else {
-                            const int r = models_det_gepp(ma, ca, ha, hca, ta, k, c2, N);
+                            const int r = models_det_gepp(ma, ca, ha, ta, k, c2, N);
                             bad = (r == 2);
                             s = bad ? 0 : r;
                             fb32 += a.pivoted ? 0u : 1u;
@@ -737,7 +749,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                                 return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
                                                        lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
                             },
-                            [&] { return hs_of(k); });
+                            hs_gepp);
                         s = d.sign;
                         bad = d.bad;
 #endif
@@ -1141,8 +1153,8 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
         x.ia2 = 1.0 / (al * al);
         x.ib2 = 1.0 / (be * be);
         x.krho = k * rh;
-        x.mu = x.krho * (be * be);   // (k rho) beta^2, as layer_elem_root forms it
-        x.pad = 0.0;
+        x.b2 = 2.0 * (be * be);      // mu = (k rho) beta^2 (lc_mu), as layer_elem_root forms it
+        x.aux = 0.0;
         lc[e] = x;
         vel[2 * e] = al;
         vel[2 * e + 1] = be;
