@@ -224,10 +224,15 @@ __device__ __forceinline__ void sqrt_rsqrt(double q, double &x, double &rx)
 // table covers th < 354.97; the index is clamped so a NaN argument stays in bounds).
 __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, unsigned tab)
 {
-    const double t = fma(th, kExpInvD, kShifter);
-    const double md = t - kShifter;
+    // th + 1.5 * 2^52 d rounds th to the nearest multiple of d (ulp d); its low word is m.
+    // Three DADDs with immediate operands (no constant materialisation); r is exact
+    // (md is within a factor 2 of th, or 0).
+    static_assert(kExpD * 16.0 == 1.0, "shifter below assumes d = 1/16");
+    constexpr double kShifterD = kShifter * kExpD;        // 1.5 * 2^48 (low word zero)
+    const double t = th + kShifterD;
+    const double md = t - kShifterD;                       // m d
     const unsigned m = min((unsigned)__double2loint(t), (unsigned)(kExpTabN - 1));
-    const double r = fma(md, -kExpD, th);                  // exact
+    const double r = th - md;                              // exact
     const double u = r * r;
     double pe = fma(kExpE2_0, u, c_expE2[1]);              // E / r^2
     double po = fma(kExpO3_0, u, c_expO3[1]);              // O / r
@@ -1183,6 +1188,17 @@ struct SignOut {
 // exponent field of |x| (0 for zero/denormal, 0x7ff for Inf/NaN)
 __device__ __forceinline__ int exp_of(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
 
+// (mag_key, above: (exponent << 20) | top 20 mantissa bits of |x|, one LOP3 where exp_of
+// needs two.)
+// BlockSignU's certificate in key units (integer pipe, ~7 instructions per node fewer than
+// exponent fields): key(max|W'|) - key(d) <= kBlockMultExp << 20, i.e. the exponent
+// difference is at most kBlockMultExp and at most kBlockMultExp - 1 unless the top mantissa
+// bits of W' do not exceed d's (|W| < 2^13, typically <= 2^12: never looser than BlockSign's
+// exponent test); and every p nonzero normal and finite:
+// key(p) - key(DBL_MIN) < key(Inf) - key(DBL_MIN) as unsigned.
+constexpr int kKeyMultMax = kBlockMultExp << 20;
+constexpr unsigned kKeyNormMin = 0x00100000u, kKeyRange = 0x7ff00000u - 0x00100000u;
+
 // State of one block-recursion sign evaluation (see det_sign_block).
 struct BlockSign {
     Elem P;                 // the previous layer's element
@@ -1289,7 +1305,8 @@ struct BlockSignU {
     ElemU P;                // the previous layer's element
     double s11, s12, s22;   // S^_t
     unsigned sgn;
-    int worst, dmin, dmax;  // as BlockSign (dmin / dmax over p_t)
+    int worst;              // max over nodes of key(max|W'|) - key(d)
+    unsigned prange;        // max over nodes of key(p) - kKeyNormMin (unsigned)
     double x11, x12, x22, rg;
 
     __device__ __forceinline__ void init(const ElemU &E)
@@ -1299,9 +1316,8 @@ struct BlockSignU {
         s12 = E.g12;
         s22 = E.g22;
         sgn = 0u;
-        worst = -4096;
-        dmin = 0x7ff;
-        dmax = 0;
+        worst = -(1 << 30);
+        prange = 0u;
     }
 
     // X = d bot(P) - G^T adj(S^) G, p = D_P d
@@ -1321,11 +1337,9 @@ struct BlockSignU {
         x22 = fma(P.g22, d, -m22);
         const double p = P.D * d;
         sgn ^= (unsigned)__double2hiint(d);
-        const int ed = exp_of(d), ep = exp_of(p);
-        const int ew = max(max(exp_of(w11), exp_of(w12)), max(exp_of(w21), exp_of(w22)));
-        worst = max(worst, ew - ed);
-        dmin = min(dmin, ep);
-        dmax = max(dmax, ep);
+        const int kw = max(max(mag_key(w11), mag_key(w12)), max(mag_key(w21), mag_key(w22)));
+        worst = max(worst, kw - mag_key(d));
+        prange = max(prange, (unsigned)mag_key(p) - kKeyNormMin);
         return p;
     }
     __device__ __forceinline__ void pre() { rg = P.rr * rcp_fast(eliminate()); }
@@ -1352,7 +1366,7 @@ struct BlockSignU {
             dre = fma(z11, z22, -i11 * i22) - fma(z12, z12, -i12 * i12);
         }
         SignOut o;
-        o.ok = (worst <= kBlockMultExp) && (dmin > 0) && (dmax < 0x7ff) && (exp_of(dre) < 0x7ff);
+        o.ok = (worst <= kKeyMultMax) && (prange < kKeyRange) && (exp_of(dre) < 0x7ff);
         o.bad = false;
         const int hi = __double2hiint(dre);
         const bool neg = ((sgn >> 31) != 0) ^ (hi < 0);

@@ -664,10 +664,12 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                     H.real = __double2hiint(H.h11i) == 0;   // +0 exactly below beta_N
                     return H;
                 };
+#if !MASW_BLOCK_SIGN
                 auto hs_gepp = [&] {     // K_hs / k, as the row scan's GEPP forms it
                     const LayerConst H = load_lc_at(ha);
                     return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
                 };
+#endif
                 while (pend) {
                     const int r = half * 32 + __ffs(pend) - 1;
                     pend &= pend - 1;
