@@ -415,6 +415,7 @@ def run_ours(args):
     }
     if not args.no_extra and world == 1:
         line["other_configs"] = other_configs(masw, torch, dev)
+        line["other_configs"]["cold_vs_cached"] = cold_latency()
     if not args.no_cpu and world == 1:   # the oracle baseline runs at N = 1 only
         cores = host_cores()
         n, d, s = oracle_sample(mods, w.lam, w.c, w.ce, args.cpu_seconds, cores)
@@ -460,6 +461,46 @@ def other_configs(masw, torch, dev):
                      "dets": alg, "dets_per_s": alg / (med / 1e3),
                      "curves_per_s": 1e3 / med, "note": w.note}
     return out
+
+
+COLD_SNIPPET = r"""
+import json, os, sys, time
+t0 = time.perf_counter()
+sys.path.insert(0, os.environ["MASW_ROOT"])
+import numpy as np
+import paper_2003_02256_b200 as masw
+import synth
+w = synth.workload("maswaves")
+m = w.models
+a = [np.ascontiguousarray(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)]
+t1 = time.perf_counter()
+masw.masw_curve(*a, w.lam, w.c)
+t2 = time.perf_counter()
+ts = []
+for _ in range(20):
+    s = time.perf_counter()
+    masw.masw_curve(*a, w.lam, w.c)
+    ts.append(time.perf_counter() - s)
+ts.sort()
+print(json.dumps({"first_call_ms": (t2 - t1) * 1e3, "cached_call_ms": ts[len(ts) // 2] * 1e3,
+                  "import_ms": (t1 - t0) * 1e3}))
+"""
+
+
+def cold_latency():
+    """the first call in a fresh process (library load, CUDA context, module
+    load) vs the cached calls after it -- the analog of the paper's first-run vs cached GPU
+    timings.  C2 through the C ABI with host buffers, wall clock."""
+    env = dict(os.environ, MASW_ROOT=ROOT)
+    try:
+        r = subprocess.run([sys.executable, "-c", COLD_SNIPPET], capture_output=True, text=True,
+                           timeout=300, env=env)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, never fatal
+        return {"error": str(e)[:200]}
+    d["note"] = ("C2 (40 lambda x 1000 c) host buffers, fresh process, wall clock; first call "
+                 "includes CUDA context creation and module load (PAPER.md:236 first-run vs cached)")
+    return d
 
 
 def main():

@@ -9,6 +9,7 @@ passage it follows in the C source.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 import threading
@@ -192,6 +193,39 @@ def det_grid_kappa(h, alpha, beta, rho, lam, c, nthreads: int | None = None):
     lib().oracle_det_grid_kappa(N, *[p for _, p in args], plam, L, pc, V, kap.ctypes.data_as(_D),
                                 sts.ctypes.data_as(_I32), nthreads or default_threads())
     return kap
+
+
+def classify_change(h, alpha, beta, rho, lam, c_lo, c_hi, iters: int = 40):
+    """P10 (reading S21): is the sign change of Re det K in (c_lo, c_hi] a
+    ROOT (a dispersion-curve point) or a POLE (an element's D_e -> 0, a clamped-layer
+    resonance)?  Bisection on sgn Re det (O6) for `iters` halvings; near a simple root
+    |Re det| shrinks ~1 bit per halving, near a simple pole it grows ~1 bit per halving, so
+    the change of log2|Re det| at the bracket ends tells them apart.  A diagnostic: reported,
+    not gated (the scan's semantics stay "first sign change").
+
+    Returns (kind, c_star, dlog2) with kind in {"root", "pole", "undecided"}."""
+    def sgn_log(c):
+        m, e, st = det(h, alpha, beta, rho, lam, c)
+        if st != 0 or m.real == 0.0:
+            return 0.0, -math.inf
+        return math.copysign(1.0, m.real), math.log2(abs(m.real)) + e
+
+    s_lo, l_lo = sgn_log(c_lo)
+    s_hi, l_hi = sgn_log(c_hi)
+    if s_lo == s_hi:
+        raise ValueError("no sign change of Re det in the bracket")
+    l0 = max(l_lo, l_hi)
+    lo, hi = float(c_lo), float(c_hi)
+    for _ in range(iters):
+        mid = 0.5 * (lo + hi)
+        s, l = sgn_log(mid)
+        if s == s_lo:
+            lo, l_lo = mid, l
+        else:
+            hi, l_hi = mid, l
+    d = max(l_lo, l_hi) - l0
+    kind = "root" if d < -0.5 * iters else ("pole" if d > 0.5 * iters else "undecided")
+    return kind, 0.5 * (lo + hi), d
 
 
 # ---------------------------------------------------------------- O7..O10

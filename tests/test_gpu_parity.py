@@ -192,6 +192,25 @@ def test_rayleigh_and_no_change_rows(masw, orc):
     assert alg == 11
 
 
+def test_pole_first_rows(masw, orc):
+    """Reading S21 / P10: a soft layer whose clamped-layer poles (D_0 -> 0) come before the
+    first root when the grid starts above its shear velocity.  The f-free recursion carries
+    1/D_0 as a ratio: same first-change index as the oracle at every wavelength,
+    through the row and the model-major kernels."""
+    h, al, be, rh = [10.0], [200.0, 700.0], [100.0, 350.0], [1800.0, 2000.0]
+    c = 100.5 + 0.25 * np.arange(400, dtype=np.float64)
+    lam = np.array([0.5, 1.0, 1.5, 2.0, 3.0, 5.0, 8.0])
+    st, ct, idx = masw.masw_curve(h, al, be, rh, lam, c)
+    ost, oct_, oidx, _ = orc.curve(h, al, be, rh, lam, c)
+    assert st == ost and np.array_equal(idx, oidx) and np.array_equal(ct, oct_)
+    assert orc.classify_change(h, al, be, rh, 1.0, c[oidx[1] - 1], c[oidx[1]])[0] == "pole"
+    M = 64
+    H = np.tile(np.array(h), (M, 1))
+    A, B, R = (np.tile(np.array(x), (M, 1)) for x in (al, be, rh))
+    res = masw.masw_curves_ensemble(H, A, B, R, lam, c, flags=masw.SCHED_MODELS)
+    assert np.array_equal(np.asarray(res.idx), np.tile(oidx, (M, 1)))
+
+
 @pytest.mark.parametrize("N", [1, 3, 10, 24, 64])
 def test_identical_stack_any_depth(masw, N):
     b = 200.0

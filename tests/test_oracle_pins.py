@@ -442,6 +442,50 @@ def test_P9_extended_grid_matches_pointwise(orc):
 
 # ------------------------------------------------------------------ P11 curve asymptotes
 
+# P10 / reading S21: root or pole.  A soft layer (beta 100 m/s, 10 m) under a scan that starts
+# above its shear velocity: its clamped-layer resonances (D -> 0, element entries -> inf) come
+# first, interlaced with the system's roots.
+SOFT_POLE = dict(h=[10.0], alpha=[200.0, 700.0], beta=[100.0, 350.0], rho=[1800.0, 2000.0])
+
+
+def soft_pole_grid():
+    return 100.5 + 0.25 * np.arange(400, dtype=np.float64)
+
+
+@pytest.mark.parametrize("lam", [2.0, 10.0, 40.0])
+def test_P10_fundamental_mode_changes_are_roots(orc, lam):
+    """On the C2 model the first sign change is the fundamental mode: a root, |det| -> 0."""
+    w = synth.workload("maswaves")
+    m = w.models
+    a = (m.h[0], m.alpha[0], m.beta[0], m.rho[0])
+    st, ct, idx, _ = orc.curve(*a, np.array([lam]), w.c)
+    j = int(idx[0])
+    kind, cs, d = orc.classify_change(*a, lam, w.c[j - 1], w.c[j])
+    assert kind == "root" and w.c[j - 1] < cs <= w.c[j] and d < -30
+
+
+def test_P10_pole_first_is_an_element_singularity(orc):
+    """The first change of the soft-layer model is a POLE, and there the layer element blows
+    up (D_0 -> 0) while at the next change -- a root -- it stays moderate."""
+    a = (SOFT_POLE["h"], SOFT_POLE["alpha"], SOFT_POLE["beta"], SOFT_POLE["rho"])
+    c, lam = soft_pole_grid(), 1.0
+    st, m, e, _ = orc.det_grid(*a, np.array([lam]), c)
+    s = np.sign(m[0].real)
+    ch = np.nonzero(s[1:] != s[:-1])[0] + 1
+    st, ct, idx, _ = orc.curve(*a, np.array([lam]), c)
+    assert idx[0] == ch[0]                                            # O7 on this grid
+    k = 2.0 * math.pi / lam
+    kinds, mags = [], []
+    for j in ch[:4]:
+        kind, cs, d = orc.classify_change(*a, lam, c[j - 1], c[j])
+        kinds.append(kind)
+        el = orc.layer_element(a[0][0], a[1][0], a[2][0], a[3][0], k, cs)
+        mags.append(np.abs(el).max())
+    assert kinds[0] == "pole" and "root" in kinds[1:]
+    r = kinds.index("root")
+    assert mags[0] > 1e9 * mags[r]
+
+
 def test_P11_short_wavelength_tends_to_top_layer_rayleigh(orc):
     m = synth.maswaves_model()
     grid = synth.maswaves_grid()
