@@ -780,8 +780,15 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
         }
         __syncwarp();   // the next item rewrites this warp's constants
     }
-    if (a.team_dets && lane == 0)
+    if (a.team_dets && lane == 0) {
+#ifdef MASW_TAIL_PROBE   // measurement build (scripts/tail_probe.py): warp finish times
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.team_dets[(long long)blockIdx.x * (blockDim.x / 32) + warp] = t;
+#else
         a.team_dets[(long long)blockIdx.x * (blockDim.x / 32) + warp] = team_alg;
+#endif
+    }
 
     my_alg = warp_sum_u64(my_alg);
     my_eval = warp_sum_u64(my_eval);
