@@ -48,6 +48,10 @@ struct ScanArgs {
     unsigned long long *team_dets;  // per-team algorithmic det counts (nullable)
     int stable;          // MASW_STABLE: the scaled, cancellation-free element (row kernel)
     int pivoted;         // MASW_PIVOTED: every sign by the banded GEPP (no block recursion)
+    // model-major scan only (set by its launcher): the last tail_models models are queued
+    // as finer work items of tail_rows wavelengths, so the warps finish closer together
+    int64_t tail_models;
+    int tail_rows;
 };
 
 // grid_mask bit: the call uses the stable element, range guard k h <= 700 instead of 350

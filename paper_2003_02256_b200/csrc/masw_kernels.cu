@@ -465,6 +465,14 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 #define MASW_MODELS_UNROLL 1
 #endif
 constexpr int kModelRows = 64;
+#ifndef MASW_TAIL_ROWS
+#define MASW_TAIL_ROWS 8
+#endif
+#ifndef MASW_TAIL_ITEMS
+#define MASW_TAIL_ITEMS 2
+#endif
+constexpr int kTailRows = MASW_TAIL_ROWS;            // wavelengths per tail piece
+constexpr int64_t kTailItemsPerWarp = MASW_TAIL_ITEMS;
 // ONE CTA per SM: one copy of the 89 KB cosh/sinh table serves all of its warps; as many
 // warps as the per-warp caches leave room for, up to kModelsBlock / 32 (16 for N <= 6).
 #ifndef MASW_MODELS_BLOCK
@@ -538,7 +546,11 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     const int64_t M = a.mod.M, L = a.L;
     const int V = (int)a.V;                 // < 2^31 (idx is int32; checked by the C ABI)
     const int64_t groups = (L + kModelRows - 1) / kModelRows;
-    const int64_t items = M * groups;
+    const int64_t Mt = a.tail_models, Mh = M - Mt;       // finer items for the last Mt models
+    const int tr = a.tail_rows > 0 ? a.tail_rows : kModelRows;
+    const int64_t groups_t = (L + tr - 1) / tr;
+    const int64_t items_h = Mh * groups;
+    const int64_t items = items_h + Mt * groups_t;
     const double *__restrict__ cg = a.c;
     const int nv = 2 * (N + 1);
     unsigned long long my_alg = 0, my_eval = 0, team_alg = 0, my_fb = 0;
@@ -549,9 +561,18 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
         if (lane == 0) item = (long long)atomicAdd(&ws->queue, 1ull);
         item = __shfl_sync(FULL, item, 0);
         if (item >= items) break;
-        const int64_t m = item / groups;
-        const int64_t i0 = (item - m * groups) * kModelRows;
-        const int nr = (int)min((int64_t)kModelRows, L - i0);
+        int64_t m, i0;
+        int nr;
+        if (item < items_h) {
+            m = item / groups;
+            i0 = (item - m * groups) * kModelRows;
+            nr = (int)min((int64_t)kModelRows, L - i0);
+        } else {
+            const int64_t it = item - items_h, q = it / groups_t;
+            m = Mh + q;
+            i0 = (it - q * groups_t) * tr;
+            nr = (int)min((int64_t)tr, L - i0);
+        }
 
         // model constants without the wavenumber: h, 1/alpha^2, 1/beta^2, rho, beta^2
         for (int e = lane; e <= N; e += 32) {
@@ -1007,7 +1028,17 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
     if (blocks < 1) blocks = 1;
     if (warps_out) *warps_out = blocks * wpc;
     if (dry) return cudaSuccess;
-    kern<<<(unsigned)blocks, 32 * wpc, smem, st>>>(a);
+    // Tail: a work item (one model's wavelengths) takes a warp ~1 ms on C5, so the warps
+    // finished up to one item apart (measured: 0.55 ms average idle, 1.4 % of the scan).  The
+    // last kTailItemsPerWarp items per warp are queued as kTailRows-wavelength pieces.
+    ScanArgs b = a;
+    b.tail_models = 0;
+    b.tail_rows = 0;
+    if (a.L > kTailRows) {
+        b.tail_models = std::min<int64_t>(a.mod.M, kTailItemsPerWarp * blocks * wpc);
+        b.tail_rows = kTailRows;
+    }
+    kern<<<(unsigned)blocks, 32 * wpc, smem, st>>>(b);
     count_launch();
     return cudaGetLastError();
 }

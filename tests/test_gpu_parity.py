@@ -361,6 +361,19 @@ def test_models_kernel_bitwise_equals_row_kernel(masw, L):
     assert np.array_equal(rows[3], mm[3])
 
 
+def test_models_kernel_tail_pieces_bitwise(masw):
+    """More models than the tail split covers (2 pieces per resident warp: 4736 models on 148
+    SMs x 16 warps): main items (all wavelengths of a model) and tail pieces (8 wavelengths)
+    in one launch give the row scan's results bit for bit."""
+    w = synth.workload("ensemble", M=6000)
+    rows = _ens(masw, w.models, w.lam, w.c, w.ce, masw.SCHED_ROWS)
+    mm = _ens(masw, w.models, w.lam, w.c, w.ce, masw.SCHED_MODELS, device=True)
+    assert rows[0] == mm[0]
+    assert np.array_equal(rows[2], mm[2])
+    assert np.array_equal(rows[1], mm[1], equal_nan=True)
+    assert np.array_equal(rows[3], mm[3])
+
+
 @pytest.mark.parametrize("N", [1, 3, 7])
 def test_models_kernel_bitwise_any_depth(masw, N):
     """Random N-layer ensembles (N = 7 is the deepest whose per-warp cache fits the one-CTA
