@@ -126,9 +126,10 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU oracle timing
 
-def oracle_sample(models, lam, c, ce, target_s: float, nthreads: int, start: int = 0):
+def oracle_sample(models, lam, c, ce, target_s: float, nthreads: int, start: int = 0,
+                  idx_out=None):
     """Run the oracle on consecutive models from `start` until ~target_s of wall time.
-    Returns (n_models, alg_dets, seconds)."""
+    Returns (n_models, alg_dets, seconds); `idx_out` (a list) receives the oracle's idx rows."""
     import oracle
 
     oracle.build()
@@ -141,6 +142,8 @@ def oracle_sample(models, lam, c, ce, target_s: float, nthreads: int, start: int
         hi = min(lo + batch, M)
         o = oracle.ensemble(models.slice(lo, hi), lam, c, ce, nthreads=nthreads)
         dets += int(o["ndet"].sum())
+        if idx_out is not None:
+            idx_out.append(np.asarray(o["idx"]))
         done += hi - lo
         el = time.perf_counter() - t0
         if el >= target_s:
@@ -418,11 +421,23 @@ def run_ours(args):
         line["other_configs"]["cold_vs_cached"] = cold_latency()
     if not args.no_cpu and world == 1:   # the oracle baseline runs at N = 1 only
         cores = host_cores()
-        n, d, s = oracle_sample(mods, w.lam, w.c, w.ce, args.cpu_seconds, cores)
+        oidx = []
+        n, d, s = oracle_sample(mods, w.lam, w.c, w.ce, args.cpu_seconds, cores, idx_out=oidx)
         line["cpu_baseline"] = {"value": d / s, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": f"first {n} models of the C5 ensemble "
                                           f"({d} algorithmic dets in {s:.1f} s; CPU: {cpu_model()})",
                                 "curves_per_s": n / s}
+        # the timed run's results checked against the oracle on the same sample
+        # (the idx of the last timed e2e step; one grid step is allowed only at near-roots,
+        # reading S16 -- the parity tests apply that rule, here mismatches are just counted)
+        o = np.concatenate(oidx, axis=0)[: min(n, Mr)]
+        g = hidx.numpy()[: o.shape[0]]
+        diff = np.abs(g.astype(np.int64) - o.astype(np.int64))
+        line["parity_check"] = {"models": int(o.shape[0]), "rows": int(o.size),
+                                "idx_equal": int((diff == 0).sum()),
+                                "idx_one_step": int((diff == 1).sum()),
+                                "idx_other": int((diff > 1).sum()),
+                                "against": "oracle (dense complex LU), cpu_baseline sample"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
