@@ -275,10 +275,16 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 && !stable &&
                             (((ex.flags & MASW_SCHED_MODELS) && models_scan_suitable(sa, dev, true)) ||
                              (ex.team == 0 && models_scan_suitable(sa, dev, false)));
+        // pair scan for single curves of many wavelengths (auto unless a team size, a static
+        // schedule or MASW_SCHED_ROWS is requested; MASW_SCHED_PAIRS forces it for M == 1)
+        const bool pairs = !models && !(ex.flags & MASW_SCHED_ROWS) &&
+                           (((ex.flags & MASW_SCHED_PAIRS) && pairs_scan_suitable(sa, dev, true)) ||
+                            (ex.team == 0 && pairs_scan_suitable(sa, dev, false)));
         const bool stats = (ex.flags & MASW_TEAM_STATS) != 0 && !(ex.flags & MASW_ASYNC);
         long long nteams = 0;
         if (stats) {
-            nteams = models ? scan_models_warps(sa, dev) : scan_teams(sa, team, dev);
+            nteams = models ? scan_models_warps(sa, dev)
+                            : (pairs ? scan_pairs_warps(sa, dev) : scan_teams(sa, team, dev));
             if (nteams <= 0) return MASW_E_CUDA;
             sa.team_dets = arena.alloc<unsigned long long>((size_t)nteams);
             CK(cudaMemsetAsync(sa.team_dets, 0, nteams * sizeof(unsigned long long), st));
@@ -292,6 +298,8 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         }
         if (models) {
             CK(launch_scan_models(sa, st, dev));
+        } else if (pairs) {
+            CK(launch_scan_pairs(sa, st, dev));
         } else {
             CK(launch_scan(sa, team, st, dev));
         }

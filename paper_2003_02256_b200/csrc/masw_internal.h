@@ -77,6 +77,11 @@ int auto_team_warps(int64_t rows, int64_t V, int device);
 // Model-major scan (ensembles): suitable when there are many (model, wavelength-block) items
 // and the per-warp caches fit two CTAs per SM; same outputs as launch_scan.
 bool models_scan_suitable(const ScanArgs &a, int device, bool forced);
+// pair scan (single curves of many wavelengths, two rows per warp in lockstep)
+bool pairs_scan_suitable(const ScanArgs &a, int device, bool forced);
+cudaError_t launch_scan_pairs(const ScanArgs &a, cudaStream_t st, int device,
+                              long long *warps_out = nullptr);
+long long scan_pairs_warps(const ScanArgs &a, int device);
 cudaError_t launch_scan_models(const ScanArgs &a, cudaStream_t st, int device,
                                long long *warps_out = nullptr);
 long long scan_models_warps(const ScanArgs &a, int device);

@@ -823,6 +823,234 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     }
 }
 
+// ------------------------------------------------------------------ pair scan (one long curve)
+// Single curves with many wavelengths (C3, C4): a warp pops TWO consecutive rows of the one
+// model and scans them in lockstep -- each lane evaluates both rows at its velocity with the
+// model-major kernel's interleaved pair evaluation (det_sign_block_u_pair), so the
+// wavelength-free terms (the 2N wave roots, the half-space factor, 1/c^2) are computed once
+// per lane, chunk and PAIR instead of once per determinant.  Adjacent rows of a sorted curve
+// stop at nearby indices (identical rows for C3), so the lockstep costs little; once one row
+// has found its change the other continues alone.  Each determinant uses the row scan's
+// operations in the row scan's order: bitwise-identical results (tests).
+constexpr int kPairBlock = 512;   // one CTA (one table copy) of 16 warps per SM, 128 registers
+
+__host__ __device__ inline unsigned pair_smem_bytes(int N)
+{
+    return (unsigned)kExpTabBytes + round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +
+                                            2u * (unsigned)(N + 1) * (unsigned)sizeof(double));
+}
+
+// GEPP sign for one lane of the pair scan (roots formed on the fly, as the row scan forms them)
+static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, unsigned ta,
+                                                 double k, double c2, int N)
+{
+    const DetOut d = det_core<false, 0, 1>(
+        N,
+        [&](int e) {
+            const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+            return layer_elem_root(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
+                                   wave_root(fma(-c2, M.ib2, 1.0)), c2, ta);
+        },
+        [&] {
+            const LayerConst H = load_lc_at(ha);
+            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
+        });
+    return d.bad ? 2 : d.sign;
+}
+
+__global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_abort;
+
+    const int N = a.mod.N;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *tab = smem;
+    LayerConst *mc = reinterpret_cast<LayerConst *>(smem + kExpTabBytes);
+    double *vel = reinterpret_cast<double *>(smem + kExpTabBytes + (unsigned)(N + 1) * sizeof(LayerConst));
+
+    Workspace *ws = a.ws;
+    if (threadIdx.x == 0) {
+        const bool bad = ws_invalid(ws, a.grid_mask, true);
+        s_abort = bad;
+        if (bad && blockIdx.x == 0) ws->abort = 1;
+    }
+    __syncthreads();
+    if (s_abort) return;
+    exp_scale_fill(tab, ws_exp_rows(ws));
+    // the one model's k-free constants (as the model-major scan fills them)
+    for (int e = threadIdx.x; e <= N; e += blockDim.x) {
+        const double al = a.mod.alpha[e], be = a.mod.beta[e], rh = a.mod.rho[e];
+        LayerConst x;
+        x.kh = (e < N) ? a.mod.h[e] : 0.0;
+        x.ia2 = 1.0 / (al * al);
+        x.ib2 = 1.0 / (be * be);
+        x.krho = rh;
+        x.b2 = 2.0 * (be * be);
+        x.aux = (e < N) ? rh / a.mod.rho[e + 1] : (rh * (be * be)) / a.mod.rho[N - 1];
+        mc[e] = x;
+        vel[2 * e] = al;
+        vel[2 * e + 1] = be;
+    }
+    __syncthreads();
+    const unsigned ta = opaque(smem_addr(tab));
+    const unsigned ma = opaque(smem_addr(mc));
+    const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
+
+    const int64_t L = a.L;
+    const int V = (int)a.V;
+    const double *__restrict__ cg = a.c;
+    const int nv = 2 * (N + 1);
+    unsigned long long my_alg = 0, my_eval = 0, team_alg = 0, my_fb = 0;
+    unsigned my_status = 0;
+
+    for (;;) {
+        long long r0;
+        if (lane == 0) r0 = (long long)atomicAdd(&ws->queue, 2ull);
+        r0 = __shfl_sync(FULL, r0, 0);
+        if (r0 >= L) break;
+        const bool two = r0 + 1 < L;
+        const double k0 = kTwoPi / a.lam[r0];                 // reading S2
+        const double k1 = two ? kTwoPi / a.lam[r0 + 1] : k0;
+        int carry0 = 0, carry1 = 0;
+        bool pend0 = true, pend1 = two;
+        for (int base = 0; base < V && (pend0 || pend1); base += 32) {
+            const int j = base + lane;
+            const bool valid = j < V;
+            double c = cg[valid ? j : V - 1];
+            {   // reading S4, as in scan_kernel
+                const double clo = __shfl_sync(FULL, c, 0) - 1e-3;
+                const double chi = __shfl_sync(FULL, c, 31) + 1e-3;
+                bool lane_near = false;
+                for (int e0 = 0; e0 < nv; e0 += 32) {
+                    bool in = false;
+                    if (e0 + lane < nv) {
+                        const double v = vel[e0 + lane];
+                        in = (v > clo) && (v < chi);
+                    }
+                    for (unsigned b = __ballot_sync(FULL, in); b; b &= b - 1)
+                        lane_near |= fabs(c - vel[e0 + __ffs(b) - 1]) < kPerturbTol;
+                }
+                if (lane_near) c = perturb_velocity(vel, nv, c);
+            }
+            const double c2 = c * c;
+            const double ic2 = rcp_fast(c2);
+            int s0 = 0, s1 = 0;
+            bool bad0 = false, bad1 = false;
+            if (valid) {
+                const LayerConst Hl = load_lc_at(ha);
+                const HalfSpace H = halfspace_k(halfspace_root(Hl.ia2, Hl.ib2, c2), Hl.aux * ic2);
+                if (pend0 && pend1) {
+                    SignOut o0, o1;
+                    det_sign_block_u_pair<MASW_MODELS_UNROLL>(
+                        N,
+                        [&](int e, ElemU &E0, ElemU &E1) {
+                            const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+                            layer_elem_root2_u(M, k0, k1, wave_root(fma(-c2, M.ia2, 1.0)),
+                                               wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta, E0,
+                                               E1);
+                        },
+                        [&](HalfSpace &H0, HalfSpace &H1) {
+                            H0 = H;
+                            H1 = H;
+                        },
+                        o0, o1);
+                    if (o0.ok) {
+                        s0 = o0.sign;
+                    } else {
+                        const int rr = pair_det_gepp(ma, ha, ta, k0, c2, N);
+                        bad0 = (rr == 2);
+                        s0 = bad0 ? 0 : rr;
+                        ++my_fb;
+                    }
+                    if (o1.ok) {
+                        s1 = o1.sign;
+                    } else {
+                        const int rr = pair_det_gepp(ma, ha, ta, k1, c2, N);
+                        bad1 = (rr == 2);
+                        s1 = bad1 ? 0 : rr;
+                        ++my_fb;
+                    }
+                    my_eval += 2;
+                } else {
+                    const double k = pend0 ? k0 : k1;
+                    const SignOut o = det_sign_block_u<MASW_MODELS_UNROLL>(
+                        N,
+                        [&](int e) {
+                            const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+                            return layer_elem_root_u(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
+                                                     wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta);
+                        },
+                        [&] { return H; });
+                    int s = 0;
+                    bool bad = false;
+                    if (o.ok) {
+                        s = o.sign;
+                    } else {
+                        const int rr = pair_det_gepp(ma, ha, ta, k, c2, N);
+                        bad = (rr == 2);
+                        s = bad ? 0 : rr;
+                        ++my_fb;
+                    }
+                    if (pend0) { s0 = s; bad0 = bad; } else { s1 = s; bad1 = bad; }
+                    ++my_eval;
+                }
+            }
+            // first-sign-change bookkeeping of one row for this chunk (as scan_kernel, TEAM 1)
+            auto settle = [&](long long r, int s, bool bad, int &carry, bool &pend) {
+                int sprev = __shfl_up_sync(FULL, s, 1);
+                if (lane == 0) sprev = carry;
+                const bool ev = valid && (bad || (j > 0 && s != sprev));
+                const unsigned mask = __ballot_sync(FULL, ev);
+                if (mask) {
+                    const int first = base + (__ffs(mask) - 1);
+                    if (j == first) {
+                        if (bad) {
+                            a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                            if (a.idx) a.idx[r] = -2;
+                            my_status |= 2u;
+                        } else {
+                            a.ct[r] = cg[j];
+                            if (a.idx) a.idx[r] = (int32_t)j;
+                        }
+                        my_alg += (unsigned long long)(j + 1);
+                    }
+                    team_alg += (unsigned long long)(first + 1);
+                    pend = false;
+                }
+                carry = __shfl_sync(FULL, s, 31);
+            };
+            if (pend0) settle(r0, s0, bad0, carry0, pend0);
+            if (pend1) settle(r0 + 1, s1, bad1, carry1, pend1);
+        }
+        for (int q = 0; q < 2; ++q) {
+            const bool p = q ? pend1 : pend0;
+            if (!p) continue;
+            team_alg += (unsigned long long)V;
+            if (lane == 0) {
+                const long long r = r0 + q;
+                a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                if (a.idx) a.idx[r] = -1;
+                my_status |= 1u;
+                my_alg += (unsigned long long)V;
+            }
+        }
+    }
+    if (a.team_dets && lane == 0)
+        a.team_dets[(long long)blockIdx.x * (blockDim.x / 32) + warp] = team_alg;
+
+    my_alg = warp_sum_u64(my_alg);
+    my_eval = warp_sum_u64(my_eval);
+    my_fb = warp_sum_u64(my_fb);
+    my_status = __reduce_or_sync(FULL, my_status);
+    if (lane == 0) {
+        if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
+        if (my_eval) atomicAdd(&ws->eval_dets, my_eval);
+        if (my_fb) atomicAdd(&ws->fallback_dets, my_fb);
+        if (my_status) atomicOr(&ws->row_status, my_status);
+    }
+}
+
 // Per-device launch facts, cached: SM count and resident CTAs per SM per (kernel, smem).
 namespace {
 std::mutex g_cache_mu;
@@ -1057,6 +1285,66 @@ bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
     long long w = 0;
     if (launch_models(a, nullptr, device, &w, true, &per_sm) != cudaSuccess) return false;
     return per_sm >= 1;
+}
+
+// Pair scan launcher: single curves (M == 1) of many wavelengths.  *warps_out: warps launched.
+static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
+                                long long *warps_out, bool dry)
+{
+    const size_t smem = pair_smem_bytes(a.mod.N);
+    auto kern = scan_pair_kernel;
+    const int sms = sm_count(device);
+    const long long key = ((long long)device << 48) | (2ll << 45) | (long long)smem;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        auto it = g_occ_cache.find(key);
+        if (it != g_occ_cache.end()) per_sm = it->second;
+    }
+    if (per_sm == 0) {
+        if (ensure_smem_optin(kern, device, 4) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPairBlock, smem) !=
+                cudaSuccess) {
+            cudaGetLastError();
+            per_sm = -1;
+        }
+        if (per_sm == 0) per_sm = -1;
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        g_occ_cache[key] = per_sm;
+    }
+    if (per_sm < 0) return cudaErrorInvalidConfiguration;
+    const int wpc = kPairBlock / 32;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = ((a.L + 1) / 2 + wpc - 1) / wpc;
+    if (need < blocks) blocks = need;
+    if (blocks < 1) blocks = 1;
+    if (warps_out) *warps_out = blocks * wpc;
+    if (dry) return cudaSuccess;
+    kern<<<(unsigned)blocks, kPairBlock, smem, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+bool pairs_scan_suitable(const ScanArgs &a, int device, bool forced)
+{
+    // one model, the queue schedule, the plain element; unless forced: at least 4 rows per
+    // resident warp (the row scan's TEAM = 1 regime; shorter curves want teams for latency)
+    if (a.mod.M != 1 || a.sched != 0 || a.stable || a.pivoted) return false;
+    if (!forced && a.L < 4ll * sm_count(device) * (kPairBlock / 32)) return false;
+    long long w = 0;
+    return launch_pairs(a, nullptr, device, &w, true) == cudaSuccess;
+}
+
+cudaError_t launch_scan_pairs(const ScanArgs &a, cudaStream_t st, int device, long long *warps_out)
+{
+    return launch_pairs(a, st, device, warps_out, false);
+}
+
+long long scan_pairs_warps(const ScanArgs &a, int device)
+{
+    long long w = 0;
+    if (launch_pairs(a, nullptr, device, &w, true) != cudaSuccess) return -1;
+    return w;
 }
 
 cudaError_t launch_scan_models(const ScanArgs &a, cudaStream_t st, int device,

@@ -26,6 +26,7 @@ SCHED_CONTIGUOUS, SCHED_MODULAR, TEAM_STATS = 0x4, 0x8, 0x10
 SCHED_ROWS, SCHED_MODELS = 0x20, 0x40   # force the row / model-major scan kernel
 STABLE = 0x80   # cancellation-free, exponentially scaled element (f3), k h <= 700
 PIVOTED = 0x100   # every scan sign by the banded GEPP (validation / A-B)
+SCHED_PAIRS = 0x200   # force the pair scan (one model: two wavelengths per warp in lockstep)
 MAX_LAYERS = 64
 
 

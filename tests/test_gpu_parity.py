@@ -374,6 +374,41 @@ def test_models_kernel_tail_pieces_bitwise(masw):
     assert np.array_equal(rows[3], mm[3])
 
 
+@pytest.mark.parametrize("name,kw", [("realistic", {}), ("uniform", {"tier": 30.0}),
+                                     ("maswaves", {}), ("tiny", {})])
+def test_pair_kernel_bitwise_equals_row_kernel(masw, name, kw):
+    """The pair scan (two wavelengths of the one model per warp, lockstep, shared roots) gives
+    the row scan's C_t and idx bit for bit and the same algorithmic count -- on the full-size
+    single-curve configs it is selected automatically, on the small ones forced."""
+    w = synth.workload(name, **kw)
+    a = [dev(x[0]) for x in (w.models.h, w.models.alpha, w.models.beta, w.models.rho)]
+    lam, c = dev(w.lam), dev(w.c)
+    st_r, ct_r, idx_r = masw.masw_curve(*a, lam, c, flags=masw.SCHED_ROWS)
+    alg_r, _ = masw.masw_last_work()
+    st_p, ct_p, idx_p = masw.masw_curve(*a, lam, c, flags=masw.SCHED_PAIRS | masw.TEAM_STATS)
+    alg_p, ev_p = masw.masw_last_work()
+    assert st_r == st_p
+    assert torch.equal(idx_r, idx_p) and torch.equal(ct_r.isnan(), ct_p.isnan())
+    assert torch.equal(torch.nan_to_num(ct_r), torch.nan_to_num(ct_p))
+    assert alg_r == alg_p and ev_p >= alg_p
+    assert int(masw.masw_last_team_dets().sum()) >= alg_p
+
+
+def test_pair_kernel_odd_rows_and_no_change(masw, orc):
+    """Odd wavelength counts (a lone last row), rows without a change, a lone pending row of a
+    pair: same results as the oracle."""
+    b = 200.0
+    al = b * math.sqrt(3.0)
+    lam = np.array([5.0, 10.0, 20.0, 0.7, 3.0])
+    c = np.linspace(150.0, 190.0, 81)
+    st, ct, idx = masw.masw_curve([1.0, 2.0], [al, 1.2 * al, al], [b, 1.2 * b, b],
+                                  [1900.0] * 3, lam, c, flags=masw.SCHED_PAIRS)
+    ost, oct_, oidx, _ = orc.curve([1.0, 2.0], [al, 1.2 * al, al], [b, 1.2 * b, b],
+                                   [1900.0] * 3, lam, c)
+    assert st == ost and np.array_equal(idx, oidx)
+    assert np.array_equal(np.nan_to_num(ct), np.nan_to_num(oct_))
+
+
 @pytest.mark.parametrize("N", [1, 3, 7])
 def test_models_kernel_bitwise_any_depth(masw, N):
     """Random N-layer ensembles (N = 7 is the deepest whose per-warp cache fits the one-CTA
