@@ -347,6 +347,11 @@ def run_ours(args):
         e2e_ms.append(e0.elapsed_time(e1))
     barrier()
 
+    # ---- C3 scaling study (BASELINE configs[2]): one N=10 curve, lambda sharded modularly
+    #      (PAPER.md:124), strong (10k lambda in total) and weak (10k per GPU); every rank
+    #      takes part, device time max over ranks, all-gather of C_t/idx included
+    c3 = uniform_scaling(masw, torch, dist, D, world, rank, dev, barrier) if not args.no_extra else None
+
     # ---- max over ranks, job totals
     tot = torch.tensor([sum(step_ms), sum(e2e_ms), sum(scan_ms)], dtype=torch.float64, device=dev)
     dets = torch.tensor([float(sum(algs))], dtype=torch.float64, device=dev)
@@ -416,6 +421,8 @@ def run_ours(args):
         "step_ms": [round(x, 3) for x in step_ms],
         "scan_ms": [round(x, 3) for x in scan_ms],
     }
+    if c3 is not None:
+        line["uniform_scaling"] = c3
     if not args.no_extra and world == 1:
         line["other_configs"] = other_configs(masw, torch, dev)
         line["other_configs"]["cold_vs_cached"] = cold_latency()
@@ -442,6 +449,44 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def uniform_scaling(masw, torch, dist, D, world, rank, dev, barrier, reps=3):
+    """C3 at this GPU count: strong (10k lambda split over the ranks) and weak (10k lambda
+    per rank) scaling of one curve through distributed.curve_sharded (modular partition,
+    per-rank C ABI call, NCCL all-gather, inverse permutation)."""
+    w = synth.workload("uniform", tier=200.0)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+    m = w.models
+    model = tuple(t(x[0]) for x in (m.h, m.alpha, m.beta, m.rho))
+    c = t(w.c)
+    ops = D.cuda_ops()
+    out = {"workload": "C3 uniform N=10, lambda = 200 m, 10k test velocities",
+           "partition": "modular (PAPER.md:124)"}
+    for mode, L in (("strong", 10_000), ("weak", 10_000 * world)):
+        lam = torch.full((L,), 200.0, dtype=torch.float64, device=dev)
+        for _ in range(2):
+            D.curve_sharded(model, lam, c, ops=ops)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dets = 0
+        for _ in range(reps):
+            D.curve_sharded(model, lam, c, ops=ops)
+            dets += masw.masw_last_work()[0]
+        e1.record()
+        barrier()
+        tt = torch.tensor([e0.elapsed_time(e1), float(dets)], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = tt.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            tt[0] = mx[0]
+        ms, d = tt.tolist()
+        out[mode] = {"wavelengths": L, "ms_per_curve": ms / reps, "dets_per_s": d / (ms / 1e3),
+                     "curves_per_s": reps / (ms / 1e3)}
+    return out
 
 
 def other_configs(masw, torch, dev):

@@ -50,6 +50,26 @@ def partition_wavelengths(W: int, s: int, strategy: str = "modular") -> List[Lis
     raise ValueError(f"unknown strategy {strategy!r}")
 
 
+_INDEX_CACHE: dict = {}
+
+
+def partition_index(W: int, s: int, rank: int, strategy: str, device) -> tuple:
+    """(this rank's wavelength indices, the concatenated order of all ranks' indices) as
+    int64 tensors on `device` -- partition_wavelengths as device index vectors, built once
+    per (W, s, rank, strategy, device) (a 10k-entry Python list per call cost ~1 ms)."""
+    key = (W, s, rank, strategy, str(device))
+    hit = _INDEX_CACHE.get(key)
+    if hit is not None:
+        return hit
+    parts = partition_wavelengths(W, s, strategy)
+    mine = torch.as_tensor(parts[rank], dtype=torch.int64).to(device)
+    order = torch.as_tensor([i for p in parts for i in p], dtype=torch.int64).to(device)
+    if len(_INDEX_CACHE) > 64:
+        _INDEX_CACHE.clear()
+    _INDEX_CACHE[key] = (mine, order, [len(p) for p in parts])
+    return _INDEX_CACHE[key]
+
+
 def shard_bounds(M: int, world: int, rank: int):
     """Contiguous model block [lo, hi) of `rank` (earlier ranks take the extra model)."""
     base, extra = divmod(M, world)
@@ -160,17 +180,15 @@ def curve_sharded(model, lam: torch.Tensor, c, ce=None, strategy: str = "modular
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     W = lam.shape[0]
-    parts = partition_wavelengths(W, world, strategy)
-    mine = torch.as_tensor(parts[rank], dtype=torch.int64, device=lam.device)
+    mine, order, counts = partition_index(W, world, rank, strategy, lam.device)
     st, ct, idx = ops.curve(*model, lam[mine], c)
     if world > 1:
         st_t = torch.tensor([st], dtype=torch.int64, device=ct.device)
         sts = _all_gather_padded(st_t, [1] * world, group)
         st = int(sts.min()) if int(sts.min()) < 0 else int(sts.max())
-    counts = [len(p) for p in parts]
     ct_g = _all_gather_padded(ct, counts, group)
     idx_g = _all_gather_padded(idx, counts, group)
-    order = torch.as_tensor([i for p in parts for i in p], dtype=torch.int64, device=ct_g.device)
+    order = order.to(ct_g.device)
     ct_full = torch.empty_like(ct_g)
     idx_full = torch.empty_like(idx_g)
     ct_full[order] = ct_g
