@@ -126,6 +126,19 @@ def ensemble_models(M: int = 100_000, seed: int = ENSEMBLE_SEED) -> Models:
     return Models(h, alpha, beta, rho)
 
 
+def random_models(M: int, N: int, seed: int) -> Models:
+    """Property-test models beyond the configs' shapes, PCG64(seed): per model and layer
+    β ~ U(60, 500) m/s in any order (reversals, stiff lids, soft channels), Poisson ratios
+    through α = β·U(1.6, 3.5), h ~ U(0.3, 8) m, ρ ~ U(1500, 2300) kg/m³."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    beta = rng.uniform(60.0, 500.0, (M, N + 1))
+    alpha = beta * rng.uniform(1.6, 3.5, (M, N + 1))
+    h = rng.uniform(0.3, 8.0, (M, N))
+    rho = rng.uniform(1500.0, 2300.0, (M, N + 1))
+    return Models(np.ascontiguousarray(h), np.ascontiguousarray(alpha),
+                  np.ascontiguousarray(beta), np.ascontiguousarray(rho))
+
+
 def tiny_lambdas() -> np.ndarray:
     return geom(60.0, 2.0, 20)
 

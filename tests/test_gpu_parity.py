@@ -488,6 +488,36 @@ def test_models_kernel_oracle_parity(masw, orc):
         assert parity.misfit_ok(orc, ct[m], w.ce, mis[m])
 
 
+@pytest.mark.parametrize("N,seed", [(1, 101), (2, 102), (3, 103), (5, 105), (8, 108)])
+def test_random_models_parity_all_kernels(masw, orc, N, seed):
+    """Random layered models outside the configs' shapes (reversals, stiff lids, wide Poisson
+    range; synth.random_models): C_t of the model-major, row and pair scans against the oracle
+    under the S16 rule, and the three scans bitwise equal to each other.  The grid starts at
+    0.3 x the smallest shear velocity (no root or pole lies below ~0.87 beta_min, and the direct
+    element formulas are well conditioned there, reading S15; the ill-conditioned start of the
+    configs' 0.5 m/s grids is covered by test_gpu_stable.py::test_small_c_false_change)."""
+    mods = synth.random_models(160, N, seed)
+    lam = synth.geom(60.0, 0.8, 24)
+    c0 = 0.3 * float(mods.beta.min())
+    c = c0 + 0.5 * np.arange(1000, dtype=np.float64)
+    o = orc.ensemble(mods, lam, c, None)
+    st_m, ct_m, idx_m, _ = _ens(masw, mods, lam, c, None, masw.SCHED_MODELS, device=True)
+    st_r, ct_r, idx_r, _ = _ens(masw, mods, lam, c, None, masw.SCHED_ROWS, device=True)
+    assert st_m == st_r == o["status"]
+    assert np.array_equal(idx_m, idx_r) and np.array_equal(ct_m, ct_r, equal_nan=True)
+    bad = 0
+    for m in range(mods.n_models):
+        if np.array_equal(idx_m[m], o["idx"][m]):
+            continue
+        ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), lam, c, idx_m[m], o["idx"][m])
+        bad += int((~ok).sum())
+    assert bad == 0
+    for m in range(0, mods.n_models, 40):   # the pair scan on single curves of these models
+        a = [dev(x[m]) for x in (mods.h, mods.alpha, mods.beta, mods.rho)]
+        st_p, ct_p, idx_p = masw.masw_curve(*a, dev(lam), dev(c), flags=masw.SCHED_PAIRS)
+        assert np.array_equal(idx_p.cpu().numpy(), idx_r[m])
+
+
 def test_models_kernel_no_change_rows_and_stats(masw, orc):
     """Rows without a sign change (idx -1, status WARN) on a grid ending below C_t, V not a
     multiple of 32, per-warp det counts summing to the algorithmic count."""

@@ -139,3 +139,25 @@ def test_stable_ensemble_matches_default_and_oracle(masw, orc):
         a = (mods.h[m], mods.alpha[m], mods.beta[m], mods.rho[m])
         ok, exact, one = parity.ct_acceptable(orc, a, w.lam, w.c, r.idx[m], o["idx"][m])
         assert ok.all()
+
+
+def test_small_c_false_change(masw, orc):
+    """Reading S15 at its extreme: a thin stiff lid (beta 491 m/s, 0.77 m) on a soft half-space
+    (beta 81 m/s) scanned from c = 0.5 m/s (c / beta_lid = 0.001, k h = 0.08).  50-digit
+    mpmath puts Re det K at +1.04e32 at c = 0.5, 1.0 and 1.5 m/s (no sign change there); the
+    direct App. A formulas cancel to ~u (beta / c)^4 / (k h)^4 relative error, so the default
+    scan's fp64 signs are unreliable at those first velocities (it reports a change at index 1
+    on this model; the fp64 oracle happens to keep the sign).  The stable element (f3,
+    MASW_STABLE) gets the true first change, as the oracle does."""
+    import mpmath  # noqa: F401
+
+    mods = synth.random_models(160, 1, 101)
+    a = tuple(x[28] for x in (mods.h, mods.alpha, mods.beta, mods.rho))
+    lam = synth.geom(60.0, 0.8, 24)[:2]
+    c = 0.5 * (np.arange(1000, dtype=np.float64) + 1.0)
+    for cj in c[:3]:
+        for l in lam:
+            assert float(_mp_det(*a, float(l), float(cj), k_double=True).real) > 1e31
+    st, ct, idx = masw.masw_curve(*a, lam, c, flags=masw.STABLE)
+    ost, oct_, oidx, _ = orc.curve(*a, lam, c)
+    assert st == ost == 0 and list(idx) == list(oidx) == [161, 161]
