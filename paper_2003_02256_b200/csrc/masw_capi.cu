@@ -272,7 +272,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
                     (ex.flags & MASW_PIVOTED) != 0};
         // model-major scan for ensembles (auto unless a team size, a static schedule or
         // MASW_SCHED_ROWS is requested; MASW_SCHED_MODELS forces it where it fits)
-        const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 && !stable &&
+        const bool models = !(ex.flags & MASW_SCHED_ROWS) && sched == 0 &&
                             (((ex.flags & MASW_SCHED_MODELS) && models_scan_suitable(sa, dev, true)) ||
                              (ex.team == 0 && models_scan_suitable(sa, dev, false)));
         // pair scan for single curves of many wavelengths (auto unless a team size, a static

@@ -605,6 +605,75 @@ __device__ __forceinline__ Elem layer_elem_stable(const LayerConst &L, double c2
     return elem_from_triples(t[0], t[1], t[2], t[3], t[4], t[5], L.krho, lc_mu(L), c2);
 }
 
+// The stable element without its factor (ElemU, as layer_elem_u for the direct one): the
+// scaled brackets and the scaled D^ are one consistent pair (f^ D^ = k rho c^2), so U = the
+// brackets with k12's correction as kappa D^ -- the f-free recursion runs on them unchanged,
+// and every entry stays O(1) for k h up to 700 (no overflow in D_t d_t either).
+__device__ __forceinline__ ElemU elemu_stable_hh(double kh, double c2, double ia2, double ib2,
+                                                 double kap, double rratio, unsigned tab)
+{
+    const double a = c2 * ia2, b = c2 * ib2;
+    double r, rr, s, rsn;
+    sqrt_rsqrt(1.0 - a, r, rr);
+    sqrt_rsqrt(1.0 - b, s, rsn);
+    const double rs = r * s;
+    const double w = fma(-a, b, a + b) * rcp_fast(1.0 + rs);          // 1 - rs
+    const double dl = 0.5 * kh * ((b - a) * rcp_fast(r + s));          // (th_r - th_s)/2
+    const ExpScaled R = exp_scaled(kh * r, tab), S = exp_scaled(kh * s, tab);
+    const ExpScaled Dl = exp_scaled(dl, tab);
+    const double es2 = S.e * S.e;
+    const double sd2 = Dl.s * Dl.s;
+    const double sdcd2 = 2.0 * Dl.s * Dl.c;
+    const double csig = fma(S.c, Dl.c, S.s * Dl.s);
+    const double ssig = fma(S.s, Dl.c, S.c * Dl.s);
+    ElemU U;
+    U.D = fma((w * w) * (rr * rsn), R.s * S.s, -4.0 * sd2 * es2);
+    U.g11 = rsn * fma(w * R.s, S.c, -sdcd2 * es2);
+    U.g12 = fma(kap, U.D, fma(2.0 * sd2, es2, w * (R.s * S.s)));
+    U.g13 = rsn * (S.e * fma(2.0 * csig, Dl.s, -w * R.s));
+    U.g14 = -2.0 * ssig * Dl.s * S.e;
+    U.g22 = rr * fma(sdcd2, es2, w * (R.c * S.s));
+    U.g24 = -rr * fma(2.0 * csig * Dl.s, S.e, w * S.s * R.e);
+    U.rr = rratio;
+    return U;
+}
+
+__device__ __forceinline__ ElemU elemu_stable_ht(double kh, double c2, double ia2, double ib2,
+                                                 double kap, double rratio, unsigned tab)
+{
+    double r, rr;
+    sqrt_rsqrt(fma(-c2, ia2, 1.0), r, rr);
+    const double qb = fma(-c2, ib2, 1.0);
+    const ExpScaled R = exp_scaled(kh * r, tab);
+    const double Cr = R.c, XSr = r * R.s, SXr = R.s * rr, er = R.e;
+    double Cs, XSs, SXs;
+    wave_trig(qb, kh, Cs, XSs, SXs);
+    ElemU U;
+    U.D = fma(SXr, SXs, fma(XSr, XSs, 2.0 * fma(-Cr, Cs, er)));
+    U.g11 = fma(Cr, SXs, -XSr * Cs);
+    U.g12 = fma(kap, U.D, fma(-XSr, XSs, fma(Cr, Cs, -er)));
+    U.g13 = fma(-er, SXs, XSr);
+    U.g14 = fma(er, Cs, -Cr);
+    U.g22 = fma(SXr, Cs, -Cr * XSs);
+    U.g24 = fma(er, XSs, -SXr);
+    U.rr = rratio;
+    return U;
+}
+
+// layer_elem_stable without the factor; L.kh = k h (row scan) -- the model-major and pair
+// scans pass a copy with k h formed from their k-free h (the same product).
+__device__ __forceinline__ ElemU layer_elemu_stable(const LayerConst &L, double c2, double ic2,
+                                                    unsigned tab)
+{
+    const double qa = fma(-c2, L.ia2, 1.0), qb = fma(-c2, L.ib2, 1.0);
+    const double kap = lc_kappa(L, ic2);
+    if (qa > 0.0 && qb > 0.0) return elemu_stable_hh(L.kh, c2, L.ia2, L.ib2, kap, L.aux, tab);
+    if (qa > 0.0) return elemu_stable_ht(L.kh, c2, L.ia2, L.ib2, kap, L.aux, tab);
+    double t[6];   // both trigonometric: bounded functions, the direct formulas
+    waves_general(qa, qb, L.kh, t, tab);
+    return elemu_from_triples(t[0], t[1], t[2], t[3], t[4], t[5], kap, L.aux);
+}
+
 // -------------------------------------------------------------- wavelength-free terms
 // The square roots r_e = sqrt(1 - c^2/alpha_e^2), s_e = sqrt(1 - c^2/beta_e^2) and the
 // half-space's k-free factors depend on the model and c but NOT on the wavelength, so the

@@ -347,11 +347,12 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
                 so.ok = false;
                 if (!a.pivoted) {
                     if constexpr (STABLE) {
-                        so = det_sign_block<MASW_LAYER_UNROLL>(
-                            N, [&](int e) { return layer_elem_stable(load_lc(lc + e), c2, ta); },
+                        const double ic2 = rcp_fast(c2);
+                        so = det_sign_block_u<MASW_LAYER_UNROLL>(
+                            N, [&](int e) { return layer_elemu_stable(load_lc(lc + e), c2, ic2, ta); },
                             [&] {
                                 const LayerConst H = load_lc(lc + N);
-                                return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
+                                return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.aux * ic2);
                             });
                     } else {
                         const double ic2 = rcp_fast(c2);
@@ -497,6 +498,14 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
 
 // GEPP sign for one lane of the model-major kernel (see row_det_gepp); the same element
 // and half-space evaluation as the kernel's hot path.
+// LayerConst of a k-free model with k h formed for one wavelength (the row scan's kh field)
+__device__ __forceinline__ LayerConst with_kh(LayerConst M, double kh)
+{
+    M.kh = kh;
+    return M;
+}
+
+template <bool STABLE>
 static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, unsigned ha,
                                                    unsigned ta, double k,
                                                    double c2, int N)
@@ -505,8 +514,9 @@ static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, uns
         N,
         [&](int e) {
             const unsigned o = 32u * (unsigned)e;
-            return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k, lds_v2(ca + o),
-                                   lds_v2(ca + o + 16u), c2, ta);
+            const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+            if constexpr (STABLE) return layer_elem_stable(with_kh(M, k * M.kh), c2, ta);
+            else return layer_elem_root(M, k, lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
         },
         [&] {
             const LayerConst H = load_lc_at(ha);   // as the row scan's GEPP forms it
@@ -515,6 +525,7 @@ static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, uns
     return d.bad ? 2 : d.sign;
 }
 
+template <bool STABLE>
 __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -708,9 +719,15 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                                 N,
                                 [&](int e, ElemU &E1, ElemU &E2) {
                                     const unsigned o = 32u * (unsigned)e;
-                                    layer_elem_root2_u(load_lc_at(ma + 48u * (unsigned)e), k, k2,
-                                                       lds_v2(ca + o), lds_v2(ca + o + 16u), c2,
-                                                       ic2, ta, E1, E2);
+                                    const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+                                    if constexpr (STABLE) {
+                                        E1 = layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
+                                        E2 = layer_elemu_stable(with_kh(M, k2 * M.kh), c2, ic2, ta);
+                                    } else {
+                                        layer_elem_root2_u(M, k, k2, lds_v2(ca + o),
+                                                           lds_v2(ca + o + 16u), c2, ic2, ta, E1,
+                                                           E2);
+                                    }
                                 },
                                 [&](HalfSpace &H1, HalfSpace &H2) {
                                     H1 = hs_scaled();
@@ -720,7 +737,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                             if (o1.ok) {
                                 s1 = o1.sign;
                             } else {
-                                const int rr = models_det_gepp(ma, ca, ha, ta, k, c2, N);
+                                const int rr = models_det_gepp<STABLE>(ma, ca, ha, ta, k, c2, N);
                                 bad1 = (rr == 2);
                                 s1 = bad1 ? 0 : rr;
                                 ++fb32;
@@ -728,7 +745,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                             if (o2.ok) {
                                 s2 = o2.sign;
                             } else {
-                                const int rr = models_det_gepp(ma, ca, ha, ta, k2, c2, N);
+                                const int rr = models_det_gepp<STABLE>(ma, ca, ha, ta, k2, c2, N);
                                 bad2 = (rr == 2);
                                 s2 = bad2 ? 0 : rr;
                                 ++fb32;
@@ -751,15 +768,18 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
                                 N,
                                 [&](int e) {
                                     const unsigned o = 32u * (unsigned)e;
-                                    return layer_elem_root_u(load_lc_at(ma + 48u * (unsigned)e),
-                                                             k, lds_v2(ca + o),
-                                                             lds_v2(ca + o + 16u), c2, ic2, ta);
+                                    const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+                                    if constexpr (STABLE)
+                                        return layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
+                                    else
+                                        return layer_elem_root_u(M, k, lds_v2(ca + o),
+                                                                 lds_v2(ca + o + 16u), c2, ic2, ta);
                                 },
                                 hs_scaled);
                         if (so.ok) {
                             s = so.sign;
                         } else {
-                            const int r = models_det_gepp(ma, ca, ha, ta, k, c2, N);
+                            const int r = models_det_gepp<STABLE>(ma, ca, ha, ta, k, c2, N);
                             bad = (r == 2);
                             s = bad ? 0 : r;
                             fb32 += a.pivoted ? 0u : 1u;
@@ -841,6 +861,7 @@ __host__ __device__ inline unsigned pair_smem_bytes(int N)
 }
 
 // GEPP sign for one lane of the pair scan (roots formed on the fly, as the row scan forms them)
+template <bool STABLE>
 static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, unsigned ta,
                                                  double k, double c2, int N)
 {
@@ -848,8 +869,9 @@ static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, unsig
         N,
         [&](int e) {
             const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
-            return layer_elem_root(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
-                                   wave_root(fma(-c2, M.ib2, 1.0)), c2, ta);
+            if constexpr (STABLE) return layer_elem_stable(with_kh(M, k * M.kh), c2, ta);
+            else return layer_elem_root(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
+                                        wave_root(fma(-c2, M.ib2, 1.0)), c2, ta);
         },
         [&] {
             const LayerConst H = load_lc_at(ha);
@@ -858,6 +880,7 @@ static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, unsig
     return d.bad ? 2 : d.sign;
 }
 
+template <bool STABLE>
 __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -946,9 +969,14 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                         N,
                         [&](int e, ElemU &E0, ElemU &E1) {
                             const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
-                            layer_elem_root2_u(M, k0, k1, wave_root(fma(-c2, M.ia2, 1.0)),
-                                               wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta, E0,
-                                               E1);
+                            if constexpr (STABLE) {
+                                E0 = layer_elemu_stable(with_kh(M, k0 * M.kh), c2, ic2, ta);
+                                E1 = layer_elemu_stable(with_kh(M, k1 * M.kh), c2, ic2, ta);
+                            } else {
+                                layer_elem_root2_u(M, k0, k1, wave_root(fma(-c2, M.ia2, 1.0)),
+                                                   wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta,
+                                                   E0, E1);
+                            }
                         },
                         [&](HalfSpace &H0, HalfSpace &H1) {
                             H0 = H;
@@ -958,7 +986,7 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                     if (o0.ok) {
                         s0 = o0.sign;
                     } else {
-                        const int rr = pair_det_gepp(ma, ha, ta, k0, c2, N);
+                        const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k0, c2, N);
                         bad0 = (rr == 2);
                         s0 = bad0 ? 0 : rr;
                         ++my_fb;
@@ -966,7 +994,7 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                     if (o1.ok) {
                         s1 = o1.sign;
                     } else {
-                        const int rr = pair_det_gepp(ma, ha, ta, k1, c2, N);
+                        const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k1, c2, N);
                         bad1 = (rr == 2);
                         s1 = bad1 ? 0 : rr;
                         ++my_fb;
@@ -978,8 +1006,12 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                         N,
                         [&](int e) {
                             const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
-                            return layer_elem_root_u(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
-                                                     wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta);
+                            if constexpr (STABLE)
+                                return layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
+                            else
+                                return layer_elem_root_u(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
+                                                         wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2,
+                                                         ta);
                         },
                         [&] { return H; });
                     int s = 0;
@@ -987,7 +1019,7 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                     if (o.ok) {
                         s = o.sign;
                     } else {
-                        const int rr = pair_det_gepp(ma, ha, ta, k, c2, N);
+                        const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k, c2, N);
                         bad = (rr == 2);
                         s = bad ? 0 : rr;
                         ++my_fb;
@@ -1217,9 +1249,10 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
 {
     const int wpc = models_warps(a.mod.N, device);
     const size_t smem = kExpTabBytes + (size_t)wpc * (size_t)warp_model_bytes(a.mod.N);
-    auto kern = scan_models_kernel;
+    auto kern = a.stable ? scan_models_kernel<true> : scan_models_kernel<false>;
     const int sms = sm_count(device);
-    const long long key = ((long long)device << 48) | (1ll << 47) | ((long long)wpc << 32) |
+    const long long key = ((long long)device << 48) | (1ll << 47) | (a.stable ? (1ll << 46) : 0ll) |
+                          ((long long)wpc << 32) |
                           (long long)smem;
     int per_sm = 0;
     {
@@ -1233,7 +1266,7 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
         if (wpc == 0) {
             per_sm = -1;
         } else {
-            if (ensure_smem_optin(kern, device, 1) != cudaSuccess) {
+            if (ensure_smem_optin(kern, device, a.stable ? 5 : 1) != cudaSuccess) {
                 cudaGetLastError();
                 per_sm = -1;
             } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc,
@@ -1292,9 +1325,10 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
                                 long long *warps_out, bool dry)
 {
     const size_t smem = pair_smem_bytes(a.mod.N);
-    auto kern = scan_pair_kernel;
+    auto kern = a.stable ? scan_pair_kernel<true> : scan_pair_kernel<false>;
     const int sms = sm_count(device);
-    const long long key = ((long long)device << 48) | (2ll << 45) | (long long)smem;
+    const long long key = ((long long)device << 48) | (2ll << 44) | (a.stable ? (1ll << 43) : 0ll) |
+                          (long long)smem;
     int per_sm = 0;
     {
         std::lock_guard<std::mutex> g(g_cache_mu);
@@ -1302,7 +1336,7 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
         if (it != g_occ_cache.end()) per_sm = it->second;
     }
     if (per_sm == 0) {
-        if (ensure_smem_optin(kern, device, 4) != cudaSuccess ||
+        if (ensure_smem_optin(kern, device, a.stable ? 6 : 4) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPairBlock, smem) !=
                 cudaSuccess) {
             cudaGetLastError();
@@ -1329,7 +1363,7 @@ bool pairs_scan_suitable(const ScanArgs &a, int device, bool forced)
 {
     // one model, the queue schedule, the plain element; unless forced: at least 4 rows per
     // resident warp (the row scan's TEAM = 1 regime; shorter curves want teams for latency)
-    if (a.mod.M != 1 || a.sched != 0 || a.stable || a.pivoted) return false;
+    if (a.mod.M != 1 || a.sched != 0 || a.pivoted) return false;
     if (!forced && a.L < 4ll * sm_count(device) * (kPairBlock / 32)) return false;
     long long w = 0;
     return launch_pairs(a, nullptr, device, &w, true) == cudaSuccess;
