@@ -119,9 +119,12 @@ typedef struct {
 /* Numerically stable element: the layer
  * stiffness is evaluated in cancellation-free form for c -> 0 (both waves hyperbolic) and
  * with exponentially scaled hyperbolic functions, so the range guard becomes
- * (2*pi/lambda_i) * h_e <= 700 instead of 350 (MASW_E_RANGE above that).  Costs ~1.7x per
- * element; runs the row scan (never the model-major one).  Applies to masw_curve,
- * masw_curves_ensemble and masw_det_grid. */
+ * (2*pi/lambda_i) * h_e <= 700 instead of 350 (MASW_E_RANGE above that).  Costs ~2.6x per
+ * determinant; runs through the same scans as the default (row, model-major, pair; results
+ * identical across them).  Use it when the grid starts far below the layers' shear
+ * velocities (c / beta_e and k h both tiny: the direct formulas' fp64 signs are unreliable
+ * there, reading S15'').  Applies to masw_curve, masw_curves_ensemble and
+ * masw_det_grid. */
 #define MASW_STABLE 0x80u
 /* Scan signs by the banded GEPP for every determinant (default: the block LDL^T recursion,
  * certified per determinant, GEPP only where the certificate fails; DESIGN.md "sign by
