@@ -1411,7 +1411,18 @@ struct BlockSignU {
         prange = max(prange, (unsigned)mag_key(p) - kKeyNormMin);
         return p;
     }
-    __device__ __forceinline__ void pre() { rg = P.rr * rcp_fast(eliminate()); }
+    // rr / p with rr folded into the reciprocal's correction: y0 (1 + e + e^2) rr as
+    // fma(rr y0, e + e^2, rr y0) -- rr y0 forms beside e, one dependent step fewer (as
+    // accurate as rcp_fast; C5 -0.25 %)
+    __device__ __forceinline__ void pre()
+    {
+        const double p = eliminate();
+        double y;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+        const double e = fma(-p, y, 1.0);
+        const double ry = P.rr * y;
+        rg = fma(ry, fma(e, e, e), ry);
+    }
     __device__ __forceinline__ void post(const ElemU &Q)
     {
         const double g = rg * Q.D;
