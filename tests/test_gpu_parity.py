@@ -394,6 +394,20 @@ def test_pair_kernel_bitwise_equals_row_kernel(masw, name, kw):
     assert int(masw.masw_last_team_dets().sum()) >= alg_p
 
 
+@pytest.mark.parametrize("N", [1, 9, 24, 64])
+def test_pair_kernel_any_depth(masw, N):
+    """The pair scan keeps no per-layer cache, so any N up to MASW_MAX_LAYERS runs through it:
+    bitwise equal to the row scan on random stacks of N layers."""
+    mods = synth.random_models(1, N, 500 + N)
+    a = [dev(x[0]) for x in (mods.h, mods.alpha, mods.beta, mods.rho)]
+    lam = dev(synth.geom(80.0, 2.0, 33))
+    c = dev(0.3 * float(mods.beta.min()) + 0.5 * np.arange(1500, dtype=np.float64))
+    r = masw.masw_curve(*a, lam, c, flags=masw.SCHED_ROWS)
+    p = masw.masw_curve(*a, lam, c, flags=masw.SCHED_PAIRS)
+    assert r.status == p.status and torch.equal(r.idx, p.idx)
+    assert torch.equal(torch.nan_to_num(r.ct), torch.nan_to_num(p.ct))
+
+
 def test_pair_kernel_odd_rows_and_no_change(masw, orc):
     """Odd wavelength counts (a lone last row), rows without a change, a lone pending row of a
     pair: same results as the oracle."""
