@@ -111,10 +111,11 @@ typedef struct {
  * (N <= ~8; else the row scan runs).  With MASW_TEAM_STATS a model-major "team" is a warp. */
 #define MASW_SCHED_ROWS 0x20u
 #define MASW_SCHED_MODELS 0x40u
-/* Single curves (one model) of many wavelengths run a pair scan by default: a warp scans two
- * consecutive wavelengths in lockstep, sharing the per-velocity wave roots (results identical
- * to the row scan).  MASW_SCHED_PAIRS forces it for any one-model call; MASW_SCHED_ROWS
- * forces the row scan. */
+/* Calls that do not take the model-major scan (one model, or ensembles too small for it, or
+ * N > ~8) run a pair scan when there are >= 4 rows per resident warp: a warp scans two
+ * consecutive wavelengths of one model in lockstep, sharing the per-velocity wave roots
+ * (results identical to the row scan).  MASW_SCHED_PAIRS forces it (any call with L >= 2);
+ * MASW_SCHED_ROWS forces the row scan. */
 #define MASW_SCHED_PAIRS 0x200u
 /* Numerically stable element: the layer
  * stiffness is evaluated in cancellation-free form for c -> 0 (both waves hyperbolic) and

@@ -854,10 +854,15 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
 // operations in the row scan's order: bitwise-identical results (tests).
 constexpr int kPairBlock = 512;   // one CTA (one table copy) of 16 warps per SM, 128 registers
 
+// per warp: the current model's k-free constants and layer velocities (S4)
+__host__ __device__ inline unsigned pair_warp_bytes(int N)
+{
+    return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +
+                   2u * (unsigned)(N + 1) * (unsigned)sizeof(double));
+}
 __host__ __device__ inline unsigned pair_smem_bytes(int N)
 {
-    return (unsigned)kExpTabBytes + round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +
-                                            2u * (unsigned)(N + 1) * (unsigned)sizeof(double));
+    return (unsigned)kExpTabBytes + (unsigned)(kPairBlock / 32) * pair_warp_bytes(N);
 }
 
 // GEPP sign for one lane of the pair scan (roots formed on the fly, as the row scan forms them)
@@ -889,8 +894,9 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
     const int N = a.mod.N;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *tab = smem;
-    LayerConst *mc = reinterpret_cast<LayerConst *>(smem + kExpTabBytes);
-    double *vel = reinterpret_cast<double *>(smem + kExpTabBytes + (unsigned)(N + 1) * sizeof(LayerConst));
+    unsigned char *wb = smem + kExpTabBytes + (unsigned)warp * pair_warp_bytes(N);
+    LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
+    double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
 
     Workspace *ws = a.ws;
     if (threadIdx.x == 0) {
@@ -901,40 +907,54 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
     __syncthreads();
     if (s_abort) return;
     exp_scale_fill(tab, ws_exp_rows(ws));
-    // the one model's k-free constants (as the model-major scan fills them)
-    for (int e = threadIdx.x; e <= N; e += blockDim.x) {
-        const double al = a.mod.alpha[e], be = a.mod.beta[e], rh = a.mod.rho[e];
-        LayerConst x;
-        x.kh = (e < N) ? a.mod.h[e] : 0.0;
-        x.ia2 = 1.0 / (al * al);
-        x.ib2 = 1.0 / (be * be);
-        x.krho = rh;
-        x.b2 = 2.0 * (be * be);
-        x.aux = (e < N) ? rh / a.mod.rho[e + 1] : (rh * (be * be)) / a.mod.rho[N - 1];
-        mc[e] = x;
-        vel[2 * e] = al;
-        vel[2 * e + 1] = be;
-    }
     __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
-    const unsigned ma = opaque(smem_addr(mc));
-    const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
 
-    const int64_t L = a.L;
+    const int64_t M = a.mod.M, L = a.L;
+    const int64_t pairs_per_model = (L + 1) / 2;
+    const int64_t items = M * pairs_per_model;
     const int V = (int)a.V;
     const double *__restrict__ cg = a.c;
     const int nv = 2 * (N + 1);
     unsigned long long my_alg = 0, my_eval = 0, team_alg = 0, my_fb = 0;
     unsigned my_status = 0;
+    int64_t cur_m = -1;
 
     for (;;) {
-        long long r0;
-        if (lane == 0) r0 = (long long)atomicAdd(&ws->queue, 2ull);
-        r0 = __shfl_sync(FULL, r0, 0);
-        if (r0 >= L) break;
-        const bool two = r0 + 1 < L;
-        const double k0 = kTwoPi / a.lam[r0];                 // reading S2
-        const double k1 = two ? kTwoPi / a.lam[r0 + 1] : k0;
+        // work item = (wavelength pair ip, model m), pair-major: the long wavelengths of
+        // every model first, as the row scan's lambda-major order
+        long long item;
+        if (lane == 0) item = (long long)atomicAdd(&ws->queue, 1ull);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= items) break;
+        const int64_t ip = item / M, m = item - ip * M;
+        const int64_t i0 = 2 * ip;
+        const bool two = i0 + 1 < L;
+        if (m != cur_m) {   // this model's k-free constants (as the model-major scan fills them)
+            __syncwarp();
+            for (int e = lane; e <= N; e += 32) {
+                const double al = a.mod.alpha[m * (N + 1) + e], be = a.mod.beta[m * (N + 1) + e];
+                const double rh = a.mod.rho[m * (N + 1) + e];
+                LayerConst x;
+                x.kh = (e < N) ? a.mod.h[m * N + e] : 0.0;
+                x.ia2 = 1.0 / (al * al);
+                x.ib2 = 1.0 / (be * be);
+                x.krho = rh;
+                x.b2 = 2.0 * (be * be);
+                x.aux = (e < N) ? rh / a.mod.rho[m * (N + 1) + e + 1]
+                                : (rh * (be * be)) / a.mod.rho[m * (N + 1) + N - 1];
+                mc[e] = x;
+                vel[2 * e] = al;
+                vel[2 * e + 1] = be;
+            }
+            __syncwarp();
+            cur_m = m;
+        }
+        const unsigned ma = opaque(smem_addr(mc));
+        const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
+        const long long r0 = m * L + i0;                        // output row of wavelength i0
+        const double k0 = kTwoPi / a.lam[i0];                   // reading S2
+        const double k1 = two ? kTwoPi / a.lam[i0 + 1] : k0;
         int carry0 = 0, carry1 = 0;
         bool pend0 = true, pend1 = two;
         for (int base = 0; base < V && (pend0 || pend1); base += 32) {
@@ -1313,7 +1333,9 @@ bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
     const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
     const int sms = sm_count(device);
     if (a.sched != 0) return false;
-    if (!forced && (items < 4ll * sms * 16 || a.L < 8)) return false;
+    // (>= 2 items per resident warp: measured crossover with the pair scan at ~2.1 on C5-like
+    // ensembles, scripts/ens_small.py)
+    if (!forced && (items < 2ll * sms * 16 || a.L < 8)) return false;
     int per_sm = 0;
     long long w = 0;
     if (launch_models(a, nullptr, device, &w, true, &per_sm) != cudaSuccess) return false;
@@ -1349,7 +1371,7 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
     if (per_sm < 0) return cudaErrorInvalidConfiguration;
     const int wpc = kPairBlock / 32;
     int64_t blocks = (int64_t)sms * per_sm;
-    const int64_t need = ((a.L + 1) / 2 + wpc - 1) / wpc;
+    const int64_t need = (a.mod.M * ((a.L + 1) / 2) + wpc - 1) / wpc;
     if (need < blocks) blocks = need;
     if (blocks < 1) blocks = 1;
     if (warps_out) *warps_out = blocks * wpc;
@@ -1361,10 +1383,10 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
 
 bool pairs_scan_suitable(const ScanArgs &a, int device, bool forced)
 {
-    // one model, the queue schedule, the plain element; unless forced: at least 4 rows per
-    // resident warp (the row scan's TEAM = 1 regime; shorter curves want teams for latency)
-    if (a.mod.M != 1 || a.sched != 0 || a.pivoted) return false;
-    if (!forced && a.L < 4ll * sm_count(device) * (kPairBlock / 32)) return false;
+    // the queue schedule; unless forced: at least 4 rows per resident warp (the row scan's
+    // TEAM = 1 regime; shorter curves want teams for latency)
+    if (a.sched != 0 || a.pivoted || a.L < 2) return false;
+    if (!forced && a.mod.M * a.L < 4ll * sm_count(device) * (kPairBlock / 32)) return false;
     long long w = 0;
     return launch_pairs(a, nullptr, device, &w, true) == cudaSuccess;
 }

@@ -408,6 +408,23 @@ def test_pair_kernel_any_depth(masw, N):
     assert torch.equal(torch.nan_to_num(r.ct), torch.nan_to_num(p.ct))
 
 
+@pytest.mark.parametrize("N,L", [(10, 40), (3, 7), (6, 2)])
+def test_pair_kernel_ensembles_bitwise(masw, N, L):
+    """The pair scan on ensembles (per-warp model constants, pair-major queue): N = 10 (beyond
+    the model-major cache), odd and tiny wavelength counts -- idx, C_t and misfit bitwise equal
+    to the row scan."""
+    mods = synth.random_models(300, N, 700 + N)
+    lam = synth.geom(60.0, 0.8, L)
+    c = 0.3 * float(mods.beta.min()) + 0.5 * np.arange(1200, dtype=np.float64)
+    ce = np.linspace(150.0, 100.0, L)
+    rows = _ens(masw, mods, lam, c, ce, masw.SCHED_ROWS, device=True)
+    prs = _ens(masw, mods, lam, c, ce, masw.SCHED_PAIRS, device=True)
+    assert rows[0] == prs[0]
+    assert np.array_equal(rows[2], prs[2])
+    assert np.array_equal(rows[1], prs[1], equal_nan=True)
+    assert np.array_equal(rows[3], prs[3])
+
+
 def test_pair_kernel_odd_rows_and_no_change(masw, orc):
     """Odd wavelength counts (a lone last row), rows without a change, a lone pending row of a
     pair: same results as the oracle."""
