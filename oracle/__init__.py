@@ -38,7 +38,7 @@ def build(force: bool = False) -> str:
     if (force or not os.path.exists(LIB) or
             os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(CORE))):
         cmd = ["gcc", "-std=gnu11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-               "-shared", "-pthread", "-o", LIB + ".tmp", SRC, "-lm"]
+               "-shared", "-pthread", "-o", LIB + ".tmp", SRC, "-lquadmath", "-lm"]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
     return LIB
@@ -66,6 +66,11 @@ def lib():
             L.oracle_det.argtypes = [ctypes.c_int32, _D, _D, _D, _D, ctypes.c_double,
                                      ctypes.c_double, _D, _I32]
             L.oracle_det_ld.argtypes = L.oracle_det.argtypes
+            L.oracle_det_fp64.argtypes = L.oracle_det.argtypes
+            L.oracle_det_q.argtypes = L.oracle_det.argtypes
+            L.oracle_fp64_error_bound.restype = ctypes.c_double
+            L.oracle_fp64_error_bound.argtypes = [ctypes.c_int32, _D, _D, _D, ctypes.c_double,
+                                                  ctypes.c_double]
             L.oracle_det_grid_ld.argtypes = [ctypes.c_int32, _D, _D, _D, _D, _D, ctypes.c_int64,
                                              _D, ctypes.c_int64, _D, _D, _I32, _I32,
                                              ctypes.c_int32]
@@ -158,17 +163,42 @@ def det_dense(A: np.ndarray):
     return complex(m[0], m[1]), int(e.value), st
 
 
-def det(h, alpha, beta, rho, lam, c, extended: bool = False):
+def det(h, alpha, beta, rho, lam, c, extended: bool = False, precision: str = "auto"):
     """O1–O5 at one (λ, c): returns (complex mantissa, exponent, status).
 
+    precision "auto" is the oracle's own choice (fp64, or binary128 where the fp64 error
+    bound exceeds its threshold, reading S15''); "fp64" forces the fp64 instance.
     ``extended=True`` runs the same arithmetic in long double (reading S15' audit)."""
     N = len(h)
     args = [_d(x) for x in (h, alpha, beta, rho)]
     m = np.zeros(2)
     e = ctypes.c_int32(0)
-    fn = lib().oracle_det_ld if extended else lib().oracle_det
+    if extended:
+        fn = lib().oracle_det_ld
+    else:
+        fn = {"auto": lib().oracle_det, "fp64": lib().oracle_det_fp64}[precision]
     st = fn(N, *[p for _, p in args], float(lam), float(c), m.ctypes.data_as(_D), ctypes.byref(e))
     return complex(m[0], m[1]), int(e.value), st
+
+
+def det_quad(h, alpha, beta, rho, lam, c):
+    """O1–O5 in binary128 (reading S15''): (re_hi, re_lo, im_hi, im_lo) of the mantissa,
+    exponent, status -- the mantissa to ~34 digits as two doubles per part."""
+    N = len(h)
+    args = [_d(x) for x in (h, alpha, beta, rho)]
+    m = np.zeros(4)
+    e = ctypes.c_int32(0)
+    st = lib().oracle_det_q(N, *[p for _, p in args], float(lam), float(c),
+                            m.ctypes.data_as(_D), ctypes.byref(e))
+    return tuple(float(x) for x in m), int(e.value), st
+
+
+def fp64_error_bound(h, alpha, beta, k, c):
+    """Reading S15'': u·max_e[16(β_e/c)⁴ + (α_e β_e/c²)²/(k h_e)⁴], the a-priori relative
+    error scale of an fp64 evaluation of det K at (k, c)."""
+    N = len(h)
+    args = [_d(x) for x in (h, alpha, beta)]
+    return float(lib().oracle_fp64_error_bound(N, *[p for _, p in args], float(k), float(c)))
 
 
 def det_kappa(h, alpha, beta, rho, lam, c):

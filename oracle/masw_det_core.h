@@ -2,21 +2,26 @@
  * oracle/masw_det_core.h -- TEST INFRASTRUCTURE ONLY (part of the oracle; see masw_oracle.c).
  *
  * Steps O3-O5 of the oracle (layer element, half-space element, dense assembly, dense
- * partial-pivot LU determinant), written once over a generic real type and included twice
- * by masw_oracle.c:
+ * partial-pivot LU determinant), written once over a generic real type and included three
+ * times by masw_oracle.c:
  *   REAL = double       the oracle proper (fp64, the paper's precision: cuDoubleComplex,
  *                       PAPER.md:248);
  *   REAL = long double  the same arithmetic carried in x87 extended precision, used only to
- *                       measure the fp64 oracle's own rounding error (reading S15').
- * Inputs (k, c', model) are doubles in both instances.  <tgmath.h> dispatches sqrt, cosh,
- * sinh, fabs (|z| for complex), frexp, ldexp to the right precision.
+ *                       measure the fp64 oracle's own rounding error (reading S15');
+ *   REAL = __float128   the same arithmetic in IEEE binary128 (libquadmath), used where the
+ *                       fp64 evaluation of these formulas cannot resolve the sign of det K
+ *                       (reading S15'': c^4 small against (alpha beta)^2 / (k h)^4).
+ * Inputs (k, c', model) are doubles in every instance: all three evaluate the same matrix
+ * K(fl(2 pi / lambda), c'), they differ only in the rounding of the arithmetic.
  *
- * Expects: REAL, SFX (name suffix) defined; <tgmath.h> included.
+ * Expects: REAL, SFX (name suffix) and the math macros of masw_oracle.c (OR_CSQRT, OR_CCOSH,
+ * OR_CSINH, OR_CABS, OR_CRE, OR_CIM, OR_RABS, OR_RMAX, OR_FREXP, OR_LDEXP, OR_FINITE,
+ * OR_CMPLX) and its complex type OR_CTYPE defined for that type.
  */
 #define OR_CAT2(a, b) a##_##b
 #define OR_CAT(a, b) OR_CAT2(a, b)
 #define OR_NAME(x) OR_CAT(x, SFX)
-#define CREAL_T REAL complex
+#define CREAL_T OR_CTYPE
 
 /* ------------------------------------------------------------------ O3 layer element
  * Kausel-Roesset / MASWaves layer stiffness (the paper cites the
@@ -37,12 +42,12 @@
 static void OR_NAME(layer_element)(REAL h, REAL alpha, REAL beta, REAL rho, REAL k, REAL c,
                                    CREAL_T Ke[4][4], int pw, REAL pf)
 {
-    CREAL_T r = sqrt((CREAL_T)(1.0 - (c * c) / (alpha * alpha)));
-    CREAL_T s = sqrt((CREAL_T)(1.0 - (c * c) / (beta * beta)));
+    CREAL_T r = OR_CSQRT((CREAL_T)(1.0 - (c * c) / (alpha * alpha)));
+    CREAL_T s = OR_CSQRT((CREAL_T)(1.0 - (c * c) / (beta * beta)));
     if (pw == 4) r = r * pf;
     if (pw == 5) s = s * pf;
-    CREAL_T Cr = cosh(k * r * h), Sr = sinh(k * r * h);
-    CREAL_T Cs = cosh(k * s * h), Ss = sinh(k * s * h);
+    CREAL_T Cr = OR_CCOSH(k * r * h), Sr = OR_CSINH(k * r * h);
+    CREAL_T Cs = OR_CCOSH(k * s * h), Ss = OR_CSINH(k * s * h);
     if (pw == 0) Cr = Cr * pf;
     if (pw == 1) Sr = Sr * pf;
     if (pw == 2) Cs = Cs * pf;
@@ -70,8 +75,8 @@ static void OR_NAME(layer_element)(REAL h, REAL alpha, REAL beta, REAL rho, REAL
 static void OR_NAME(halfspace_element)(REAL alpha, REAL beta, REAL rho, REAL k, REAL c,
                                        CREAL_T Kh[2][2], int pw, REAL pf)
 {
-    CREAL_T r = sqrt((CREAL_T)(1.0 - (c * c) / (alpha * alpha)));
-    CREAL_T s = sqrt((CREAL_T)(1.0 - (c * c) / (beta * beta)));
+    CREAL_T r = OR_CSQRT((CREAL_T)(1.0 - (c * c) / (alpha * alpha)));
+    CREAL_T s = OR_CSQRT((CREAL_T)(1.0 - (c * c) / (beta * beta)));
     if (pw == 4) r = r * pf;
     if (pw == 5) s = s * pf;
     REAL mu = k * rho * beta * beta;
@@ -114,14 +119,14 @@ static void OR_NAME(assemble)(int32_t N, const double *h, const double *alpha,
 static int OR_NAME(det_lu)(int n, CREAL_T *A, CREAL_T *mant, int *exp2)
 {
     for (int i = 0; i < n * n; ++i)
-        if (!isfinite(creal(A[i])) || !isfinite(cimag(A[i]))) return OR_E_NONFINITE;
+        if (!OR_FINITE(OR_CRE(A[i])) || !OR_FINITE(OR_CIM(A[i]))) return OR_E_NONFINITE;
     CREAL_T m = 1.0;
     int ex = 0;
     for (int kk = 0; kk < n; ++kk) {
         int p = kk;
-        REAL best = fabs(A[kk * n + kk]);
+        REAL best = OR_CABS(A[kk * n + kk]);
         for (int i = kk + 1; i < n; ++i) {
-            REAL v = fabs(A[i * n + kk]);
+            REAL v = OR_CABS(A[i * n + kk]);
             if (v > best) {
                 best = v;
                 p = i;
@@ -146,16 +151,16 @@ static int OR_NAME(det_lu)(int n, CREAL_T *A, CREAL_T *mant, int *exp2)
             for (int j = kk; j < n; ++j) A[i * n + j] -= l * A[kk * n + j];
         }
         m *= piv;
-        REAL t = fmax(fabs(creal(m)), fabs(cimag(m)));
-        if (!isfinite(t)) return OR_E_NONFINITE;
+        REAL t = OR_RMAX(OR_RABS(OR_CRE(m)), OR_RABS(OR_CIM(m)));
+        if (!OR_FINITE(t)) return OR_E_NONFINITE;
         if (t == 0.0) {
             *mant = 0.0;
             *exp2 = 0;
             return OR_OK;
         }
         int e2;
-        frexp(t, &e2);
-        m = ldexp(creal(m), -e2) + I * ldexp(cimag(m), -e2);
+        OR_FREXP(t, &e2);
+        m = OR_CMPLX(OR_LDEXP(OR_CRE(m), -e2), OR_LDEXP(OR_CIM(m), -e2));
         ex += e2;
     }
     *mant = m;

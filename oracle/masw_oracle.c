@@ -42,7 +42,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
-#include <tgmath.h>
+
+#include <quadmath.h>
 
 typedef double complex cplx;
 
@@ -138,20 +139,164 @@ double oracle_perturb_velocity(int32_t N, const double *alpha, const double *bet
 
 /* ------------------------------------------------------------------ O3-O5
  * The element / assembly / dense-LU steps live in masw_det_core.h, instantiated for fp64
- * (the oracle) and for long double (its rounding-error audit, reading S15').
+ * (the oracle), for long double (its rounding-error audit, reading S15') and for binary128
+ * (the points where fp64 cannot resolve the sign, reading S15'', below).  The math macros
+ * name each type's libm / libquadmath functions.
  */
 #define REAL double
+#define OR_CTYPE double complex
 #define SFX d
+#define OR_CSQRT csqrt
+#define OR_CCOSH ccosh
+#define OR_CSINH csinh
+#define OR_CABS cabs
+#define OR_CRE creal
+#define OR_CIM cimag
+#define OR_RABS fabs
+#define OR_RMAX fmax
+#define OR_FREXP frexp
+#define OR_LDEXP ldexp
+#define OR_FINITE isfinite
+#define OR_CMPLX(a, b) CMPLX(a, b)
 #include "masw_det_core.h"
 #undef REAL
+#undef OR_CTYPE
 #undef SFX
+#undef OR_CSQRT
+#undef OR_CCOSH
+#undef OR_CSINH
+#undef OR_CABS
+#undef OR_CRE
+#undef OR_CIM
+#undef OR_RABS
+#undef OR_RMAX
+#undef OR_FREXP
+#undef OR_LDEXP
+#undef OR_FINITE
+#undef OR_CMPLX
 #define REAL long double
+#define OR_CTYPE long double complex
 #define SFX ld
+#define OR_CSQRT csqrtl
+#define OR_CCOSH ccoshl
+#define OR_CSINH csinhl
+#define OR_CABS cabsl
+#define OR_CRE creall
+#define OR_CIM cimagl
+#define OR_RABS fabsl
+#define OR_RMAX fmaxl
+#define OR_FREXP frexpl
+#define OR_LDEXP ldexpl
+#define OR_FINITE isfinite
+#define OR_CMPLX(a, b) CMPLXL(a, b)
 #include "masw_det_core.h"
 #undef REAL
+#undef OR_CTYPE
 #undef SFX
+#undef OR_CSQRT
+#undef OR_CCOSH
+#undef OR_CSINH
+#undef OR_CABS
+#undef OR_CRE
+#undef OR_CIM
+#undef OR_RABS
+#undef OR_RMAX
+#undef OR_FREXP
+#undef OR_LDEXP
+#undef OR_FINITE
+#undef OR_CMPLX
+#define REAL __float128
+#define OR_CTYPE __complex128
+#define SFX q
+#define OR_CSQRT csqrtq
+#define OR_CCOSH ccoshq
+#define OR_CSINH csinhq
+#define OR_CABS cabsq
+#define OR_CRE crealq
+#define OR_CIM cimagq
+#define OR_RABS fabsq
+#define OR_RMAX fmaxq
+#define OR_FREXP frexpq
+#define OR_LDEXP ldexpq
+#define OR_FINITE finiteq
+#define OR_CMPLX(a, b) __builtin_complex((__float128)(a), (__float128)(b))
+#include "masw_det_core.h"
+#undef REAL
+#undef OR_CTYPE
+#undef SFX
+#undef OR_CSQRT
+#undef OR_CCOSH
+#undef OR_CSINH
+#undef OR_CABS
+#undef OR_CRE
+#undef OR_CIM
+#undef OR_RABS
+#undef OR_RMAX
+#undef OR_FREXP
+#undef OR_LDEXP
+#undef OR_FINITE
+#undef OR_CMPLX
 
+typedef __complex128 cplx_q;
 typedef long double complex cplx_ld;
+_Static_assert(sizeof(cplx_ld) <= sizeof(cplx_q), "scratch reuse");
+
+/* ------------------------------------------------------------------ reading S15''
+ * Where the fp64 evaluation cannot resolve the sign.  As c -> 0 (all waves evanescent) the
+ * App. A brackets are O(c^2) .. O(c^4) differences of O(cosh^2) terms: D -> a b (k h)^2 for
+ * small k h (a = c^2/alpha^2, b = c^2/beta^2), with absolute rounding ~u in cosh ~ 1, and the
+ * element's soft part is a further (k h)^2 below its stiff part; for thick layers the
+ * relative error of D tends to ~16 u (beta/c)^4.  So the relative error of an fp64 det K is
+ * of the order of
+ *     P(c, k) = u max_e [ 16 (beta_e/c)^4 + (alpha_e beta_e / c^2)^2 / (k h_e)^4 ],
+ * u = 2^-53 (measured against 60-digit mpmath on random layered models: error / P <= 30,
+ * median ~1; tests/test_oracle_pins.py pins the bound and the binary128 values).  Where
+ * P > OR_QUAD_TAU the oracle evaluates the same formulas in a wider type: x87 long double
+ * (u = 2^-64) while P 2^-11 <= OR_QUAD_TAU, else binary128 (u = 2^-113, error scale P 2^-60).
+ * So every oracle determinant has an error scale below OR_QUAD_TAU.
+ */
+static const double OR_QUAD_TAU = 1e-6;
+
+double oracle_fp64_error_bound(int32_t N, const double *h, const double *alpha,
+                               const double *beta, double k, double c)
+{
+    const double c2 = c * c, c4 = c2 * c2;
+    double worst = 0.0;
+    for (int e = 0; e < N; ++e) {
+        const double b2 = beta[e] * beta[e];
+        const double ab = alpha[e] * beta[e];
+        const double kh = k * h[e];
+        const double kh2 = kh * kh;
+        const double t = (16.0 * b2 * b2 + (ab * ab) / (kh2 * kh2)) / c4;
+        if (t > worst) worst = t;
+    }
+    return ldexp(worst, -53);
+}
+
+/* O5 at one (lambda, c) as the oracle evaluates it (reading S15''): the fp64 instance, or the
+ * long double / binary128 instance of the same formulas where P(c', k) > OR_QUAD_TAU (c' the
+ * perturbed velocity the matrix is assembled at).  Kq: scratch of n*n binary128 entries (also
+ * used as the long double scratch: sizeof(cplx_ld) <= sizeof(cplx_q)). */
+static int det_at(int32_t N, const double *h, const double *alpha, const double *beta,
+                  const double *rho, double lambda, double c, cplx *K, cplx_q *Kq, cplx *mant,
+                  int *exp2)
+{
+    const double k = OR_TWO_PI / lambda;
+    const double cp = oracle_perturb_velocity(N, alpha, beta, c);
+    const double P = oracle_fp64_error_bound(N, h, alpha, beta, k, cp);
+    if (P <= OR_QUAD_TAU) return det_at_d(N, h, alpha, beta, rho, lambda, c, K, mant, exp2);
+    if (ldexp(P, -11) <= OR_QUAD_TAU) {
+        cplx_ld ml = 0.0;
+        const int st = det_at_ld(N, h, alpha, beta, rho, lambda, c, (cplx_ld *)Kq, &ml, exp2);
+        *mant = CMPLX((double)creall(ml), (double)cimagl(ml));
+        return st;
+    }
+    cplx_q mq = 0.0;
+    const int st = det_at_q(N, h, alpha, beta, rho, lambda, c, Kq, &mq, exp2);
+    *mant = CMPLX((double)crealq(mq), (double)cimagq(mq));
+    return st;
+}
+
 
 /* Exported for the pins: Ke as 16 complex numbers, row-major, (re, im) interleaved. */
 void oracle_layer_element(double h, double alpha, double beta, double rho, double k, double c,
@@ -211,12 +356,50 @@ int oracle_det(int32_t N, const double *h, const double *alpha, const double *be
 {
     int n = 2 * (N + 1);
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    cplx_q *Kq = (cplx_q *)malloc(sizeof(cplx_q) * n * n);
+    cplx m = 0.0;
+    int e = 0;
+    int st = det_at(N, h, alpha, beta, rho, lambda, c, K, Kq, &m, &e);
+    free(K);
+    free(Kq);
+    mant2[0] = creal(m);
+    mant2[1] = cimag(m);
+    *exp2 = e;
+    return st;
+}
+
+/* The fp64 instance alone (what oracle_det returned before reading S15''; for the pins). */
+int oracle_det_fp64(int32_t N, const double *h, const double *alpha, const double *beta,
+                    const double *rho, double lambda, double c, double *mant2, int32_t *exp2)
+{
+    int n = 2 * (N + 1);
+    cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
     cplx m = 0.0;
     int e = 0;
     int st = det_at_d(N, h, alpha, beta, rho, lambda, c, K, &m, &e);
     free(K);
     mant2[0] = creal(m);
     mant2[1] = cimag(m);
+    *exp2 = e;
+    return st;
+}
+
+/* The binary128 instance alone: mantissa as (hi, lo) double pairs of re and im
+ * (mant4 = [re_hi, re_lo, im_hi, im_lo]), for the pins against mpmath. */
+int oracle_det_q(int32_t N, const double *h, const double *alpha, const double *beta,
+                 const double *rho, double lambda, double c, double *mant4, int32_t *exp2)
+{
+    int n = 2 * (N + 1);
+    cplx_q *K = (cplx_q *)malloc(sizeof(cplx_q) * n * n);
+    cplx_q m = 0.0;
+    int e = 0;
+    int st = det_at_q(N, h, alpha, beta, rho, lambda, c, K, &m, &e);
+    free(K);
+    const __float128 re = crealq(m), im = cimagq(m);
+    mant4[0] = (double)re;
+    mant4[1] = (double)(re - (__float128)mant4[0]);
+    mant4[2] = (double)im;
+    mant4[3] = (double)(im - (__float128)mant4[2]);
     *exp2 = e;
     return st;
 }
@@ -305,14 +488,14 @@ static int sign_re(cplx m)
  */
 static void scan_row(int32_t N, const double *h, const double *alpha, const double *beta,
                      const double *rho, double lambda, const double *c, int64_t V, cplx *K,
-                     double *ct, int32_t *idx, int64_t *ndet)
+                     cplx_q *Kq, double *ct, int32_t *idx, int64_t *ndet)
 {
     int64_t count = 0;
     int s_old = 0;
     for (int64_t j = 0; j < V; ++j) {
         cplx m = 0.0;
         int e;
-        int st = det_at_d(N, h, alpha, beta, rho, lambda, c[j], K, &m, &e);
+        int st = det_at(N, h, alpha, beta, rho, lambda, c[j], K, Kq, &m, &e);
         ++count;
         if (st != OR_OK) {
             *idx = OR_IDX_NONFINITE;
@@ -351,6 +534,7 @@ static void *rows_worker(void *arg)
     rows_job *J = (rows_job *)arg;
     int n = 2 * (J->N + 1);
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
+    cplx_q *Kq = (cplx_q *)malloc(sizeof(cplx_q) * n * n);
     const int64_t total = J->M * J->L;
     for (;;) {
         int64_t r = atomic_fetch_add(&J->next, 1);
@@ -359,10 +543,11 @@ static void *rows_worker(void *arg)
         int32_t N = J->N;
         int64_t nd = 0;
         scan_row(N, J->h + m * N, J->alpha + m * (N + 1), J->beta + m * (N + 1),
-                 J->rho + m * (N + 1), J->lam[i], J->c, J->V, K, &J->ct[r], &J->idx[r], &nd);
+                 J->rho + m * (N + 1), J->lam[i], J->c, J->V, K, Kq, &J->ct[r], &J->idx[r], &nd);
         if (J->ndet) J->ndet[r] = nd;
     }
     free(K);
+    free(Kq);
     return NULL;
 }
 
@@ -517,6 +702,7 @@ static void *grid_worker(void *arg)
     int n = 2 * (G->N + 1);
     cplx *K = (cplx *)malloc(sizeof(cplx) * n * n);
     cplx_ld *Kl = (cplx_ld *)malloc(sizeof(cplx_ld) * n * n);
+    cplx_q *Kq = (cplx_q *)malloc(sizeof(cplx_q) * n * n);
     for (;;) {
         int64_t i = atomic_fetch_add(&G->next, 1);
         if (i >= G->L) break;
@@ -535,7 +721,7 @@ static void *grid_worker(void *arg)
                 im = (double)cimagl(m);
             } else {
                 cplx m = 0.0;
-                st = det_at_d(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], K, &m, &e);
+                st = det_at(G->N, G->h, G->alpha, G->beta, G->rho, G->lam[i], G->c[j], K, Kq, &m, &e);
                 re = creal(m);
                 im = cimag(m);
             }
@@ -548,6 +734,7 @@ static void *grid_worker(void *arg)
     }
     free(K);
     free(Kl);
+    free(Kq);
     return NULL;
 }
 

@@ -440,6 +440,97 @@ def test_P9_extended_grid_matches_pointwise(orc):
             assert mm == mant[i, j] and ee == ex[i, j]
 
 
+# ------------------------------------------------------------------ reading S15'' (small c)
+# The oracle's precision ladder: fp64 where the a-priori error scale
+#   P(c, k) = u max_e [16 (beta_e/c)^4 + (alpha_e beta_e / c^2)^2 / (k h_e)^4]
+# is <= 1e-6, else the same formulas in long double / binary128.  Pinned against 60-digit
+# mpmath (bounds rounding, not the formula), never against the oracle itself.
+
+LID = dict(seed=101, N=1, m=28)          # thin stiff lid (beta 491 m/s, 0.77 m) on a soft half-space
+
+
+def _lid_model():
+    mods = synth.random_models(160, LID["N"], LID["seed"])
+    return tuple(x[LID["m"]] for x in (mods.h, mods.alpha, mods.beta, mods.rho))
+
+
+def _mp_sign(a, lam, c):
+    return int(np.sign(float(_mp_det(*a, lam, c, dps=60, k_double=True).real)))
+
+
+def test_S15pp_quad_instance_matches_mpmath(orc):
+    """The binary128 instance reproduces 60-digit mpmath within its own error scale
+    (40 P 2^-60, u = 2^-113 instead of 2^-53; <= 1e-15 here) at the ill-conditioned low-c
+    points, where the fp64 instance is off by tens of percent or more, and at a benign point;
+    the automatic choice has mpmath's sign there."""
+    import mpmath as mp
+
+    a = _lid_model()
+    worst_fp64 = 0.0
+    for lam, c in [(60.0, 0.5), (55.0, 1.0), (57.0, 1.5), (5.0, 0.5), (60.0, 150.0)]:
+        cp = orc.perturb_velocity(a[1], a[2], c)
+        P = orc.fp64_error_bound(a[0], a[1], a[2], 6.283185307179586 / lam, cp)
+        ex = _mp_det(*a, lam, cp, dps=60, k_double=True)
+        (rh, rl, ih, il), e, st = orc.det_quad(*a, lam, c)
+        got = mp.mpc(mp.mpf(rh) + mp.mpf(rl), mp.mpf(ih) + mp.mpf(il)) * mp.mpf(2) ** e
+        err = float(abs(got - ex) / abs(ex))
+        assert st == 0 and err <= 40.0 * P * 2.0 ** -60 + 1e-30 and err < 1e-15, (lam, c, err, P)
+        m, e2, _ = orc.det(*a, lam, c, precision="fp64")
+        worst_fp64 = max(worst_fp64, float(abs(mp.mpc(m.real, m.imag) * mp.mpf(2) ** e2 - ex) / abs(ex)))
+        ma, ea, _ = orc.det(*a, lam, c)
+        assert np.sign(ma.real) == np.sign(float(ex.real))
+    assert worst_fp64 > 0.1        # the ladder matters here: fp64 alone is not sign-safe
+
+
+def test_S15pp_bound_dominates_fp64_error(orc):
+    """P is an error SCALE for the fp64 instance: on random layered models at low c the
+    measured fp64 error never exceeds 40 P (and P rises as c falls), while every automatic
+    (laddered) oracle determinant is within 1e-5 of mpmath."""
+    import mpmath as mp
+
+    worst_ratio, worst_auto = 0.0, 0.0
+    for N, seed, mi in [(2, 102, 32), (3, 103, 4), (5, 105, 22), (8, 108, 38), (8, 108, 8)]:
+        mods = synth.random_models(40, N, seed)
+        a = tuple(x[mi] for x in (mods.h, mods.alpha, mods.beta, mods.rho))
+        for lam in (60.0, 5.0):
+            Ps = []
+            for c in (0.5, 2.0, 8.0):
+                k = 6.283185307179586 / lam
+                cp = orc.perturb_velocity(a[1], a[2], c)
+                P = orc.fp64_error_bound(a[0], a[1], a[2], k, cp)
+                Ps.append(P)
+                ex = _mp_det(*a, lam, cp, dps=60, k_double=True)
+                m, e, _ = orc.det(*a, lam, c, precision="fp64")
+                err = float(abs(mp.mpc(m.real, m.imag) * mp.mpf(2) ** e - ex) / abs(ex))
+                worst_ratio = max(worst_ratio, err / P)
+                ma, ea, _ = orc.det(*a, lam, c)
+                worst_auto = max(worst_auto, float(abs(mp.mpc(ma.real, ma.imag) * mp.mpf(2) ** ea - ex) / abs(ex)))
+            assert Ps[0] > Ps[1] > Ps[2]
+    assert worst_ratio < 40.0, worst_ratio
+    assert worst_auto < 1e-5, worst_auto
+
+
+def test_S15pp_lid_first_change_by_brute_force(orc):
+    """Algorithm 1 on the lid model from c = 0.5 m/s: the oracle's first
+    change (idx 161) is the first change of the EXACT signs -- every mpmath sign from c_0 to
+    c_160 equals sgn Re det(c_0), and c_161 differs -- while the fp64 instance alone flips at
+    the first points (its sign at c = 0.5 disagrees with mpmath's on some wavelength)."""
+    a = _lid_model()
+    c = 0.5 * (np.arange(1000, dtype=np.float64) + 1.0)
+    lam = 60.0
+    st, ct, idx, nd = orc.curve(*a, [lam], c)
+    assert st == 0 and int(idx[0]) == 161 and ct[0] == c[161]
+    s0 = _mp_sign(a, lam, orc.perturb_velocity(a[1], a[2], c[0]))
+    for j in list(range(0, 161, 8)) + [159, 160]:
+        assert _mp_sign(a, lam, orc.perturb_velocity(a[1], a[2], c[j])) == s0, j
+    assert _mp_sign(a, lam, orc.perturb_velocity(a[1], a[2], c[161])) != s0
+    flips = 0
+    for l in synth.geom(60.0, 0.8, 24)[:6]:
+        m, e, _ = orc.det(*a, l, c[0], precision="fp64")
+        flips += int(np.sign(m.real) != _mp_sign(a, l, c[0]))
+    assert flips >= 1
+
+
 # ------------------------------------------------------------------ P11 curve asymptotes
 
 # P10 / reading S21: root or pole.  A soft layer (beta 100 m/s, 10 m) under a scan that starts
