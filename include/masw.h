@@ -93,7 +93,7 @@ typedef struct {
 
 /* exec.flags */
 #define MASW_ASYNC 0x1u       /* device pointers: no status readback, return after enqueue  */
-#define MASW_TIME_SCAN 0x2u   /* record CUDA events around the scan kernel (masw_last_scan_ms) */
+#define MASW_TIME_SCAN 0x2u   /* record CUDA events around the scan (small-c prefix + scan kernel; masw_last_scan_ms) */
 /* Row schedule of the scan (default: a work-stealing queue over rows, lambda-major).  The two
  * static schedules are the paper's partitions, here over the kernel's teams:
  * team g of G takes a contiguous block of rows, or rows g, g+G, g+2G, ... (load-balance
@@ -117,15 +117,22 @@ typedef struct {
  * (results identical to the row scan).  MASW_SCHED_PAIRS forces it (any call with L >= 2);
  * MASW_SCHED_ROWS forces the row scan. */
 #define MASW_SCHED_PAIRS 0x200u
+/* Small-c prefix (reading S15'').  At very low c the direct App. A formulas
+ * cancel: the relative fp64 error of det K is of the order of
+ *   P(c, k) = 2^-53 max_e [16 (beta_e/c)^4 + (alpha_e beta_e / c^2)^2 / (k h_e)^4],
+ * so their signs are noise where P ~ 1 (e.g. a thin stiff lid scanned from 0.5 m/s).  By
+ * DEFAULT every determinant with P > 1e-3 -- a prefix of each row's ascending grid -- is
+ * evaluated with the stable element below (in a pre-pass kernel shared by every scan) and
+ * the rest with the direct element, so C_t is the first change of the exact signs for any
+ * grid start.  MASW_DIRECT skips the prefix (the direct element everywhere: A/B only). */
+#define MASW_DIRECT 0x400u
 /* Numerically stable element: the layer
  * stiffness is evaluated in cancellation-free form for c -> 0 (both waves hyperbolic) and
  * with exponentially scaled hyperbolic functions, so the range guard becomes
  * (2*pi/lambda_i) * h_e <= 700 instead of 350 (MASW_E_RANGE above that).  Costs ~2.6x per
  * determinant; runs through the same scans as the default (row, model-major, pair; results
- * identical across them).  Use it when the grid starts far below the layers' shear
- * velocities (c / beta_e and k h both tiny: the direct formulas' fp64 signs are unreliable
- * there, reading S15'').  Applies to masw_curve, masw_curves_ensemble and
- * masw_det_grid. */
+ * identical across them).  With it every determinant uses the stable element (no prefix
+ * is needed).  Applies to masw_curve, masw_curves_ensemble and masw_det_grid. */
 #define MASW_STABLE 0x80u
 /* Scan signs by the banded GEPP for every determinant (default: the block LDL^T recursion,
  * certified per determinant, GEPP only where the certificate fails; DESIGN.md "sign by
@@ -213,6 +220,11 @@ int64_t masw_last_team_dets(int64_t *out, int64_t n);
  * are not counted for -2), and the determinants actually evaluated including speculation.
  * Only filled for synchronous calls (not MASW_ASYNC); -1 otherwise. */
 int masw_last_work(int64_t *algorithmic_dets, int64_t *evaluated_dets);
+
+/* Small-c prefix (reading S15'', MASW_DIRECT) of the calling thread's last synchronous
+ * curve/ensemble call: rows with a prefix, and determinants evaluated with the stable element
+ * there.  Returns 0, or -1 if none was recorded (MASW_ASYNC, MASW_STABLE, MASW_DIRECT). */
+int masw_last_prefix(int64_t *rows, int64_t *dets);
 
 /* Of the determinants the calling thread's last synchronous scan evaluated, how many had
  * their sign re-evaluated by the banded GEPP because the block recursion's multipliers were

@@ -31,6 +31,7 @@ constexpr int kScanRing = 64;
 thread_local cudaEvent_t t_scan_ev[kScanRing][2] = {};
 thread_local long long t_scan_count = 0;   // TIME_SCAN launches recorded by this thread
 thread_local long long t_last_alg = -1, t_last_eval = -1, t_last_fb = -1;
+thread_local long long t_last_prefix_rows = -1, t_last_prefix_dets = -1;
 thread_local std::vector<long long> t_team_dets;
 thread_local long long t_team_count = -1;
 
@@ -226,6 +227,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
     if (misfit_out && !ce) return MASW_E_ARG;
     if (mod_in.M == 0) return MASW_OK;
     t_last_alg = t_last_eval = t_last_fb = -1;
+    t_last_prefix_rows = t_last_prefix_dets = -1;
     const Exec ex = resolve(exp);
     if (ex.team != 0 && (ex.team < 1 || ex.team > 16 || (ex.team & (ex.team - 1))))
         return MASW_E_ARG;
@@ -296,6 +298,14 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
             if (!slot[1]) CK(cudaEventCreate(&slot[1]));
             CK(cudaEventRecord(slot[0], st));
         }
+        // reading S15'': the rows' small-c prefixes with the stable element, before the scan
+        if (!stable && !(ex.flags & MASW_DIRECT)) {
+            int32_t *pst = arena.alloc<int32_t>((size_t)R);
+            int8_t *pca = arena.alloc<int8_t>((size_t)R);
+            CK(launch_smallc_prefix(sa, pst, pca, st, dev));
+            sa.pstart = pst;
+            sa.pcarry = pca;
+        }
         if (models) {
             CK(launch_scan_models(sa, st, dev));
         } else if (pairs) {
@@ -316,6 +326,10 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         t_last_alg = (long long)w.alg_dets;
         t_last_eval = (long long)w.eval_dets;
         t_last_fb = (long long)w.fallback_dets;
+        if (sa.pstart) {
+            t_last_prefix_rows = (long long)w.prefix_rows;
+            t_last_prefix_dets = (long long)w.prefix_dets;
+        }
         if (stats) {
             t_team_dets.assign((size_t)nteams, 0);
             CK(cudaMemcpy(t_team_dets.data(), sa.team_dets, nteams * sizeof(long long),
@@ -512,7 +526,8 @@ int masw_det_grid(const masw_model *model, const double *lambda, int64_t L, cons
         CK(cudaMemsetAsync(ws, 0, sizeof(Workspace), st));
         CK(launch_validate(mod, dlam, L, dc, V, nullptr, ws, st));
         const bool stable = (ex.flags & MASW_STABLE) != 0;
-        CK(launch_det_grid(mod, dlam, L, dc, V, dre, dim, dex, ws, st, stable));
+        CK(launch_det_grid(mod, dlam, L, dc, V, dre, dim, dex, ws, st, stable,
+                           (ex.flags & MASW_DIRECT) == 0));
         if (!host && (ex.flags & MASW_ASYNC)) return MASW_OK;
         const Workspace w = read_status(ws, st);
         const int code = decode(w, false, true, stable);
@@ -585,6 +600,13 @@ int64_t masw_last_team_dets(int64_t *out, int64_t n)
 }
 
 int64_t masw_last_fallbacks(void) { return t_last_fb; }
+
+int masw_last_prefix(int64_t *rows, int64_t *dets)
+{
+    if (rows) *rows = t_last_prefix_rows;
+    if (dets) *dets = t_last_prefix_dets;
+    return (t_last_prefix_rows < 0) ? -1 : 0;
+}
 
 int masw_last_work(int64_t *algorithmic_dets, int64_t *evaluated_dets)
 {

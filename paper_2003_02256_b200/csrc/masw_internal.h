@@ -22,6 +22,8 @@ struct Workspace {
     int abort;                         // set by the scan kernel when validation failed
     int range_bad;                     // k_max * h_max > 350
     unsigned long long fallback_dets;  // sign re-evaluated with GEPP (block recursion not certified)
+    unsigned long long prefix_rows;    // rows with a small-c prefix (reading S15''; smallc_prefix_kernel)
+    unsigned long long prefix_dets;    // determinants evaluated by smallc_prefix_kernel
 };
 
 // Model classes for Workspace::model_err
@@ -52,6 +54,12 @@ struct ScanArgs {
     // as finer work items of tail_rows wavelengths, so the warps finish closer together
     int64_t tail_models;
     int tail_rows;
+    // small-c prefix (reading S15''), written by smallc_prefix_kernel per output row m*L + i:
+    // start = first grid index the scan evaluates (the dets below it were evaluated with the
+    // stable element), or -1 when the row was finished there; carry = sgn Re det at start-1.
+    // nullptr: no prefix (MASW_STABLE / MASW_DIRECT), every row starts at 0.
+    const int32_t *pstart;
+    const int8_t *pcarry;
 };
 
 // grid_mask bit: the call uses the stable element, range guard k h <= 700 instead of 350
@@ -72,8 +80,13 @@ cudaError_t launch_argmin(const double *misfit, int64_t M, int64_t *best, double
                           cudaStream_t st);
 cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, const double *c,
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
-                            cudaStream_t st, bool stable = false);
+                            cudaStream_t st, bool stable = false, bool prefix = true);
 int auto_team_warps(int64_t rows, int64_t V, int device);
+// Reading S15'': evaluate every row's small-c prefix (grid points with c_j^4 < Q_r) with the
+// stable element, write pstart / pcarry (ScanArgs) and finish rows whose first change lies in
+// the prefix.  Runs before any scan kernel of the same call on the same stream.
+cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carry,
+                                 cudaStream_t st, int device);
 // Model-major scan (ensembles): suitable when there are many (model, wavelength-block) items
 // and the per-warp caches fit two CTAs per SM; same outputs as launch_scan.
 bool models_scan_suitable(const ScanArgs &a, int device, bool forced);

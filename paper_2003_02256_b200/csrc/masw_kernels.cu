@@ -151,6 +151,230 @@ cudaError_t launch_validate_ce(const double *ce, int64_t L, Workspace *ws, cudaS
     return launch_validate(none, nullptr, L, nullptr, 0, ce, ws, st);
 }
 
+// ------------------------------------------------------------------ small-c prefix (S15'')
+__device__ __forceinline__ unsigned long long warp_sum_u64_pre(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// Reading S15'': at very low c the direct App. A element cancels; the relative
+// rounding error of an fp64 det K is of the order of
+//   P(c, k) = u max_e [16 (beta_e/c)^4 + (alpha_e beta_e / c^2)^2 / (k h_e)^4].
+// Every det with P > tau -- i.e. c_j^4 < Q_r = (u/tau) max_e [16 beta_e^4 + (alpha_e beta_e)^2
+// / (k h_e)^4], a PREFIX of each row's ascending grid -- is evaluated with the cancellation-
+// free stable element (f3) by this kernel, before the scan; the scans evaluate the rest with
+// the direct element.  The rule depends only on (model, lambda, c_j), so every scan gives the
+// same result.  C5 (tau = 1e-3): ~1/3 of the rows have a prefix of 1-6 grid points (2.2e6 of
+// 1.03e9 dets), so the prefix dets are PACKED 32 to a warp pass (each warp takes 32 rows,
+// lays their prefix dets out contiguously and evaluates them in ceil(T / 32) passes) -- the
+// row-wise alternative (one row's 1-6 dets per warp pass) would idle 26-31 lanes.
+constexpr double kSmallCTau = 1e-3;
+constexpr double kSmallCScale = 0x1p-53 / kSmallCTau;
+
+// Q_r of model m at wavenumber k (global-memory model arrays)
+__device__ __forceinline__ double smallc_q(const ModelArgs &mod, int64_t m, double k)
+{
+    const int N = mod.N;
+    double worst = 0.0;
+    for (int e = 0; e < N; ++e) {
+        const double al = mod.alpha[m * (N + 1) + e], be = mod.beta[m * (N + 1) + e];
+        const double kh = k * mod.h[m * N + e];
+        const double b2 = be * be, ab = al * be, kh2 = kh * kh;
+        worst = fmax(worst, fma(16.0 * b2, b2, (ab * ab) / (kh2 * kh2)));
+    }
+    return kSmallCScale * worst;
+}
+
+// LayerConst of layer e of model m at wavenumber k, formed exactly as the row scan forms it
+// (K / k constants: rho, rho beta^2; only k h carries the wavelength).
+__device__ __forceinline__ LayerConst row_layer_const(const ModelArgs &mod, int64_t m, int e,
+                                                      double k)
+{
+    const int N = mod.N;
+    const double al = mod.alpha[m * (N + 1) + e];
+    const double be = mod.beta[m * (N + 1) + e];
+    const double rh = mod.rho[m * (N + 1) + e];
+    LayerConst x;
+    x.kh = (e < N) ? k * mod.h[m * N + e] : 0.0;
+    x.ia2 = 1.0 / (al * al);
+    x.ib2 = 1.0 / (be * be);
+    x.krho = rh;
+    x.b2 = 2.0 * (be * be);
+    x.aux = (e < N) ? rh / mod.rho[m * (N + 1) + e + 1] : (rh * (be * be)) / mod.rho[m * (N + 1) + N - 1];
+    return x;
+}
+
+// sgn Re det K (2: non-finite) of model m at (k, c') with the stable element: the certified
+// block recursion, the banded GEPP where it is not certified (or always, MASW_PIVOTED) --
+// what the row scan computes under MASW_STABLE.
+static __device__ __noinline__ int prefix_det_sign(ModelArgs mod, int64_t m, double k, double c,
+                                                   unsigned tab, bool pivoted)
+{
+    const int N = mod.N;
+    const double c2 = c * c;
+    if (!pivoted) {
+        const double ic2 = rcp_fast(c2);
+        const SignOut so = det_sign_block_u<1>(
+            N, [&](int e) { return layer_elemu_stable(row_layer_const(mod, m, e, k), c2, ic2, tab); },
+            [&] {
+                const LayerConst H = row_layer_const(mod, m, N, k);
+                return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.aux * ic2);
+            });
+        if (so.ok) return so.sign;
+    }
+    const DetOut d = det_core<false, 0, 1>(
+        N, [&](int e) { return layer_elem_stable(row_layer_const(mod, m, e, k), c2, tab); },
+        [&] {
+            const LayerConst H = row_layer_const(mod, m, N, k);
+            return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
+        });
+    return d.bad ? 2 : d.sign;
+}
+
+// the S4-perturbed velocity of model m (layer velocities read from global memory)
+__device__ __forceinline__ double perturb_model(const ModelArgs &mod, int64_t m, double c)
+{
+    const int N = mod.N;
+    for (;;) {
+        bool near = false;
+        for (int e = 0; e <= N; ++e)
+            near |= (fabs(c - mod.alpha[m * (N + 1) + e]) < kPerturbTol) |
+                    (fabs(c - mod.beta[m * (N + 1) + e]) < kPerturbTol);
+        if (!near) return c;
+        c = c * kPerturbFactor;
+    }
+}
+
+constexpr int kPrefixBlock = 256;
+
+__global__ void __launch_bounds__(kPrefixBlock) smallc_prefix_kernel(ScanArgs a, int32_t *pstart,
+                                                                     int8_t *pcarry)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_abort;
+    Workspace *ws = a.ws;
+    if (threadIdx.x == 0) s_abort = ws_invalid(ws, a.grid_mask, true);
+    __syncthreads();
+    if (s_abort) return;
+    exp_scale_fill(smem, ws_exp_rows(ws));
+    __syncthreads();
+    const unsigned ta = opaque(smem_addr(smem));
+
+    const int lane = threadIdx.x & 31;
+    const int64_t M = a.mod.M, L = a.L, V = a.V, R = M * L;
+    const double *__restrict__ cg = a.c;
+    const int64_t nwarps = (int64_t)gridDim.x * (kPrefixBlock / 32);
+    unsigned long long my_alg = 0, my_eval = 0, my_rows = 0;
+    unsigned my_status = 0;
+    for (int64_t b = (int64_t)blockIdx.x * (kPrefixBlock / 32) + (threadIdx.x >> 5); b * 32 < R;
+         b += nwarps) {
+        // ---- lane = one output row q = m L + i: its prefix length n = #{j : c_j^4 < Q}
+        const int64_t q = b * 32 + lane;
+        const bool valid = q < R;
+        const int64_t m = valid ? q / L : 0, i = valid ? q - m * L : 0;
+        const double k = kTwoPi / a.lam[i];                       // reading S2
+        int64_t n = 0;
+        if (valid) {
+            const double Q = smallc_q(a.mod, m, k);
+            int64_t lo = 0, hi = V;                               // first j with c_j^4 >= Q
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                const double c2 = cg[mid] * cg[mid];
+                if (c2 * c2 < Q) lo = mid + 1; else hi = mid;
+            }
+            n = lo;
+        }
+        // ---- pack the 32 rows' prefix dets: row o's dets are tasks excl_o .. excl_o + n_o - 1
+        int64_t excl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t t = __shfl_up_sync(FULL, excl, o);
+            if (lane >= o) excl += t;
+        }
+        const int64_t T = __shfl_sync(FULL, excl, 31);
+        excl -= n;
+        my_rows += (unsigned long long)__popc(__ballot_sync(FULL, n > 0));
+        bool done = false, fbad = false;
+        int64_t fj = -1;
+        int prev = 0;   // sign of the previous task (across passes)
+        for (int64_t t0 = 0; t0 < T; t0 += 32) {
+            const int64_t t = t0 + lane;
+            const bool act = t < T;
+            int o = 0;   // owner: the last lane with excl <= t (it has n > 0 when t < T)
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int64_t e = __shfl_sync(FULL, excl, o + step);
+                if (e <= t) o += step;
+            }
+            const int64_t jj = t - __shfl_sync(FULL, excl, o);
+            const int64_t mo = __shfl_sync(FULL, m, o);
+            const double ko = __shfl_sync(FULL, k, o);
+            const int64_t no = __shfl_sync(FULL, n, o);
+            int s = 0;
+            bool bad = false;
+            if (act) {
+                const double cp = perturb_model(a.mod, mo, cg[jj]);
+                const int r = prefix_det_sign(a.mod, mo, ko, cp, ta, a.pivoted != 0);
+                bad = (r == 2);
+                s = bad ? 0 : r;
+                if (jj == no - 1) pcarry[b * 32 + o] = (int8_t)s;   // the scan's carried sign
+            }
+            int sp = __shfl_up_sync(FULL, s, 1);
+            if (lane == 0) sp = prev;
+            prev = __shfl_sync(FULL, s, 31);
+            const bool ev = act && jj > 0 && (bad || s != sp);
+            for (unsigned mk = __ballot_sync(FULL, ev); mk; mk &= mk - 1) {
+                const int src = __ffs(mk) - 1;     // task order = (row, j) order
+                const int ob = __shfl_sync(FULL, o, src);
+                const int64_t jb = __shfl_sync(FULL, jj, src);
+                const bool bb = __shfl_sync(FULL, (int)bad, src) != 0;
+                if (lane == ob && !done) {
+                    done = true;
+                    fj = jb;
+                    fbad = bb;
+                }
+            }
+        }
+        my_eval += (lane == 0) ? (unsigned long long)T : 0ull;
+        if (!valid) continue;
+        if (done) {                       // first change inside the prefix (Algorithm 1)
+            pstart[q] = -1;
+            if (fbad) {
+                a.ct[q] = __longlong_as_double(0x7ff8000000000000ll);
+                if (a.idx) a.idx[q] = -2;
+                my_status |= 2u;
+            } else {
+                a.ct[q] = cg[fj];
+                if (a.idx) a.idx[q] = (int32_t)fj;
+            }
+            my_alg += (unsigned long long)(fj + 1);
+        } else if (n >= V) {              // the whole grid was the prefix: no change
+            pstart[q] = -1;
+            a.ct[q] = __longlong_as_double(0x7ff8000000000000ll);
+            if (a.idx) a.idx[q] = -1;
+            my_status |= 1u;
+            my_alg += (unsigned long long)V;
+        } else {
+            pstart[q] = (int32_t)n;       // the scan starts here (carry written above)
+            if (n == 0) pcarry[q] = 0;
+        }
+    }
+    my_alg = warp_sum_u64_pre(my_alg);
+    my_eval = warp_sum_u64_pre(my_eval);
+    my_status = __reduce_or_sync(FULL, my_status);
+    if (lane == 0) {
+        if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
+        if (my_eval) {
+            atomicAdd(&ws->eval_dets, my_eval);
+            atomicAdd(&ws->prefix_dets, my_eval);
+        }
+        if (my_rows) atomicAdd(&ws->prefix_rows, my_rows);
+        if (my_status) atomicOr(&ws->row_status, my_status);
+    }
+}
+
 // ------------------------------------------------------------------ scan
 
 template <int TEAM, int BLOCK>
@@ -246,6 +470,8 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     exp_scale_fill(tab, ws_exp_rows(ws));
     __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
+    // rows with a small-c prefix (reading S15''; smallc_prefix_kernel ran before this kernel)
+    const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;
 
     const int64_t M = a.mod.M, L = a.L, V = a.V;
     const int64_t rows = M * L;
@@ -309,10 +535,22 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
         }
         team_sync<TEAM, BLOCK>(team);
 
+        // ---- the row's small-c prefix (reading S15''): grid points below jstart were
+        //      evaluated with the stable element by smallc_prefix_kernel (sign pcs at
+        //      jstart - 1); jstart = -1: the row was finished there
+        int64_t jstart = 0;
+        int pcs = 0;
+        if (prefix) {
+            const int st = a.pstart[m * L + i];
+            if (st < 0) continue;
+            jstart = st;
+            pcs = a.pcarry[m * L + i];
+        }
+
         // ---- ascending scan in chunks of 32*TEAM velocities
-        int carry = 0;
+        int carry = pcs;
         bool found = false;
-        for (int64_t base = 0; base < V; base += 32 * TEAM) {
+        for (int64_t base = (jstart / (32 * TEAM)) * (32 * TEAM); base < V; base += 32 * TEAM) {
             const int64_t j = base + tl;
             // Reading S4 without a per-lane loop over all 2(N+1) layer velocities: the grid is
             // strictly increasing, so only velocities inside this warp's range [c_lo, c_hi]
@@ -340,7 +578,9 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
             }
             int s = 0;
             bool bad = false;
-            if (j < V) {
+            if (j < jstart) {
+                s = pcs;   // evaluated by the small-c prefix (no change there)
+            } else if (j < V) {
 #if MASW_BLOCK_SIGN
                 const double c2 = c * c;
                 SignOut so;
@@ -465,7 +705,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 #ifndef MASW_MODELS_UNROLL
 #define MASW_MODELS_UNROLL 1
 #endif
-constexpr int kModelRows = 64;
+constexpr int kModelRows = 48;   // wavelengths per work item (C5: 40, one item per model)
 #ifndef MASW_TAIL_ROWS
 #define MASW_TAIL_ROWS 8
 #endif
@@ -483,7 +723,8 @@ constexpr int kModelsBlock = MASW_MODELS_BLOCK;
 constexpr int kModelsMinWarps = 12;
 
 // Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
-// velocities (S4), k per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
+// velocities (S4), k per row, the first grid index per row (small-c prefix, reading S15''),
+// the carried sign per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
 // number of 16-byte units, so the lanes' 128-bit loads are conflict-free): the roots
 // (x_a, 1/|x_a|), (x_b, 1/|x_b|) of every layer, the half-space (r, s), (gw, t) and case.
 __host__ __device__ inline unsigned lane_cache_stride(int N) { return 32u * (unsigned)N + 48u; }
@@ -492,6 +733,7 @@ __host__ __device__ inline unsigned warp_model_bytes(int N)
     return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
                    2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
                    (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
+                   (unsigned)kModelRows * (unsigned)sizeof(int32_t) +      // first index per row
                    (unsigned)kModelRows +                                  // carried sign per row (s8)
                    32u * lane_cache_stride(N));                            // per-lane roots
 }
@@ -538,7 +780,8 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
     double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
     double *kr = vel + 2 * (N + 1);
-    signed char *carry = reinterpret_cast<signed char *>(kr + kModelRows);   // per row: last sign
+    int32_t *jst = reinterpret_cast<int32_t *>(kr + kModelRows);             // per row: first index
+    signed char *carry = reinterpret_cast<signed char *>(jst + kModelRows);  // per row: last sign
     const unsigned stride = lane_cache_stride(N);
     unsigned char *cl = reinterpret_cast<unsigned char *>(carry + kModelRows) + (unsigned)lane * stride;
 
@@ -553,6 +796,7 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     exp_scale_fill(tab, ws_exp_rows(ws));
     __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
+    const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;   // reading S15''
 
     const int64_t M = a.mod.M, L = a.L;
     const int V = (int)a.V;                 // < 2^31 (idx is int32; checked by the C ABI)
@@ -602,21 +846,46 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             vel[2 * e] = al;
             vel[2 * e + 1] = be;
         }
-        for (int r = lane; r < nr; r += 32) {
-            kr[r] = kTwoPi / a.lam[i0 + r];   // reading S2
-            carry[r] = 0;
+        // rows of the item in two 32-bit halves: pending = not yet found.  Small-c prefix
+        // (reading S15''): row r's scan starts at jst[r] with carried sign carry[r]; rows the
+        // prefix kernel finished are not pending.  smax / smin: largest / smallest start.
+        unsigned pend0 = (nr >= 32) ? ~0u : ((1u << nr) - 1u);
+        unsigned pend1 = (nr > 32) ? ((1u << (nr - 32)) - 1u) : 0u;
+        int smax = 0, smin = 0;
+        {
+            int hi = 0, lo = INT_MAX;
+            unsigned done0 = 0, done1 = 0;
+            for (int r = lane; r < nr; r += 32) {
+                kr[r] = kTwoPi / a.lam[i0 + r];   // reading S2
+                int st = 0, cs = 0;
+                if (prefix) {
+                    st = a.pstart[m * L + i0 + r];
+                    cs = a.pcarry[m * L + i0 + r];
+                }
+                jst[r] = st;
+                carry[r] = (signed char)cs;
+                if (st >= 0) {
+                    hi = max(hi, st);
+                    lo = min(lo, st);
+                }
+                const unsigned fin = __ballot_sync(__activemask(), st < 0);
+                if (r < 32) done0 = fin; else done1 = fin;
+            }
+            pend0 &= ~__shfl_sync(FULL, done0, 0);
+            pend1 &= ~__shfl_sync(FULL, done1, 0);
+            smax = __reduce_max_sync(FULL, hi);
+            smin = __reduce_min_sync(FULL, lo);
         }
         __syncwarp();
         const unsigned ma = opaque(smem_addr(mc));
         const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
         const unsigned ka = opaque(smem_addr(kr));
+        const unsigned sa = opaque(smem_addr(jst));
         const unsigned ya = opaque(smem_addr(carry));
 
-        // rows of the item in two 32-bit halves: pending = not yet found
-        unsigned pend0 = (nr >= 32) ? ~0u : ((1u << nr) - 1u);
-        unsigned pend1 = (nr > 32) ? ((nr == 64) ? ~0u : ((1u << (nr - 32)) - 1u)) : 0u;
         unsigned ev32 = 0, fb32 = 0;
-        for (int base = 0; base < V && (pend0 | pend1); base += 32) {
+        const int base0 = (pend0 | pend1) ? (smin / 32) * 32 : 0;
+        for (int base = base0; base < V && (pend0 | pend1); base += 32) {
             const int j = base + lane;
             const bool valid = j < V;
             double c = cg[valid ? j : V - 1];
@@ -654,12 +923,27 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
             }
             const unsigned ca = opaque(smem_addr(cl));
             const unsigned hca = ca + 32u * (unsigned)N;
+            // chunks below some row's small-c prefix end (reading S15''): only the rows whose
+            // scan starts before the chunk's end take part; lanes below a row's start take the
+            // prefix's sign
+            const bool slow = base < smax;
+            unsigned act0 = ~0u, act1 = ~0u;
+            if (slow) {
+                const bool a0 = lane < nr && lds_s32(sa + 4u * (unsigned)lane) < base + 32;
+                const bool a1 = lane + 32 < nr && lds_s32(sa + 4u * (unsigned)(lane + 32)) < base + 32;
+                act0 = __ballot_sync(FULL, a0);
+                act1 = __ballot_sync(FULL, a1);
+            }
 #pragma unroll 1
             for (int half = 0; half < 2; ++half) {
-                unsigned pend = half ? pend1 : pend0;
+                unsigned pend = half ? (pend1 & act1) : (pend0 & act0);
                 unsigned found = 0;
                 // first-sign-change bookkeeping of row r for this chunk (lane signs s, bad)
                 auto settle = [&](int r, int s, bool bad) {
+                    if (slow && j < lds_s32(sa + 4u * (unsigned)r)) {
+                        s = lds_s8(ya + (unsigned)r);
+                        bad = false;
+                    }
                     int sprev = __shfl_up_sync(FULL, s, 1);
                     if (lane == 0) sprev = lds_s8(ya + (unsigned)r);
                     const bool ev = valid && (bad || (j > 0 && s != sprev));
@@ -910,6 +1194,7 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
     __syncthreads();
     const unsigned ta = opaque(smem_addr(tab));
 
+    const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;   // reading S15''
     const int64_t M = a.mod.M, L = a.L;
     const int64_t pairs_per_model = (L + 1) / 2;
     const int64_t items = M * pairs_per_model;
@@ -955,9 +1240,21 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
         const long long r0 = m * L + i0;                        // output row of wavelength i0
         const double k0 = kTwoPi / a.lam[i0];                   // reading S2
         const double k1 = two ? kTwoPi / a.lam[i0 + 1] : k0;
-        int carry0 = 0, carry1 = 0;
-        bool pend0 = true, pend1 = two;
-        for (int base = 0; base < V && (pend0 || pend1); base += 32) {
+        // small-c prefixes (reading S15''): row q starts at js_q with carried sign pc_q, or
+        // was finished by smallc_prefix_kernel (js_q = -1)
+        int js0 = 0, js1 = 0, pc0 = 0, pc1 = 0;
+        if (prefix) {
+            js0 = a.pstart[r0];
+            pc0 = a.pcarry[r0];
+            if (two) {
+                js1 = a.pstart[r0 + 1];
+                pc1 = a.pcarry[r0 + 1];
+            }
+        }
+        int carry0 = pc0, carry1 = pc1;
+        bool pend0 = js0 >= 0, pend1 = two && js1 >= 0;
+        const int jlo = (pend0 && pend1) ? min(js0, js1) : (pend0 ? js0 : (pend1 ? js1 : 0));
+        for (int base = (jlo / 32) * 32; base < V && (pend0 || pend1); base += 32) {
             const int j = base + lane;
             const bool valid = j < V;
             double c = cg[valid ? j : V - 1];
@@ -1047,6 +1344,14 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                     if (pend0) { s0 = s; bad0 = bad; } else { s1 = s; bad1 = bad; }
                     ++my_eval;
                 }
+            }
+            if (j < js0) {   // evaluated by the small-c prefix
+                s0 = pc0;
+                bad0 = false;
+            }
+            if (j < js1) {
+                s1 = pc1;
+                bad1 = false;
             }
             // first-sign-change bookkeeping of one row for this chunk (as scan_kernel, TEAM 1)
             auto settle = [&](long long r, int s, bool bad, int &carry, bool &pend) {
@@ -1151,6 +1456,22 @@ size_t smem_optin_limit(int device)
     return (size_t)optin;
 }
 }  // namespace
+
+cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carry,
+                                 cudaStream_t st, int device)
+{
+    const size_t smem = kExpTabBytes;
+    cudaError_t e = ensure_smem_optin(smallc_prefix_kernel, device, 7);
+    if (e != cudaSuccess) return e;
+    const int64_t rows = a.mod.M * a.L;
+    const int64_t need = (rows + kPrefixBlock - 1) / kPrefixBlock;   // 32 rows per warp
+    int64_t blocks = 2ll * sm_count(device);
+    if (need < blocks) blocks = need;
+    if (blocks < 1) blocks = 1;
+    smallc_prefix_kernel<<<(unsigned)blocks, kPrefixBlock, smem, st>>>(a, start, carry);
+    count_launch();
+    return cudaGetLastError();
+}
 
 int auto_team_warps(int64_t rows, int64_t V, int device)
 {
@@ -1519,7 +1840,7 @@ template <bool STABLE>
 __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const double *lam,
                                                        int64_t L, const double *c, int64_t V,
                                                        double *mre, double *mim, int32_t *ex,
-                                                       const Workspace *ws)
+                                                       const Workspace *ws, bool prefix)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     if (ws_invalid(ws, 0x1Fu | (STABLE ? kGridStable : 0u), true)) return;
@@ -1546,7 +1867,11 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
     __syncthreads();
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= V) return;
-    const DetOut d = det_K<true, 0, STABLE>(lc, vel, smem_addr(tab), N, c[j]);
+    // the scans' small-c rule (reading S15''): the stable element where c_j^4 < Q
+    const double cj2 = c[j] * c[j];
+    const DetOut d = (STABLE || (prefix && cj2 * cj2 < smallc_q(mod, 0, k)))
+                         ? det_K<true, 0, true>(lc, vel, smem_addr(tab), N, c[j])
+                         : det_K<true, 0, false>(lc, vel, smem_addr(tab), N, c[j]);
     const int64_t o = i * V + j;
     mre[o] = d.mre;
     mim[o] = d.mim;
@@ -1555,7 +1880,7 @@ __global__ void __launch_bounds__(256) det_grid_kernel(ModelArgs mod, const doub
 
 cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, const double *c,
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
-                            cudaStream_t st, bool stable)
+                            cudaStream_t st, bool stable, bool prefix)
 {
     const size_t smem = kExpTabBytes + team_model_bytes(m.N);
     int dev = 0;
@@ -1564,7 +1889,7 @@ cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, co
     cudaError_t e = ensure_smem_optin(kern, dev, stable ? 3 : 2);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((V + 255) / 256), (unsigned)L);
-    kern<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws);
+    kern<<<grid, 256, smem, st>>>(m, lam, L, c, V, mre, mim, ex, ws, prefix);
     count_launch();
     return cudaGetLastError();
 }

@@ -90,14 +90,31 @@ class Ops:
 
 
 def cuda_ops(flags: int = 0, team_warps: int = 0) -> Ops:
+    """The CUDA library as per-rank compute.  A failing call (invalid model in this rank's
+    shard, out-of-range k h, ...) does NOT raise here: it returns its negative status with
+    NaN / -1 outputs, so every rank still reaches the status all-gather and the drivers raise
+    on ALL ranks together (raising on one rank would leave the others blocked in the
+    collective)."""
     from . import masw
 
     def ens(h, a, b, r, lam, c, ce):
-        res = masw.masw_curves_ensemble(h, a, b, r, lam, c, ce, flags=flags, team_warps=team_warps)
-        return res.status, res.ct, res.idx, res.misfit
+        try:
+            res = masw.masw_curves_ensemble(h, a, b, r, lam, c, ce, flags=flags,
+                                            team_warps=team_warps)
+            return res.status, res.ct, res.idx, res.misfit
+        except masw.MaswError as e:
+            M, L = h.shape[0], lam.shape[0]
+            return (e.code, _filled((M, L), float("nan"), torch.float64, lam),
+                    _filled((M, L), -1, torch.int32, lam),
+                    _filled((M,), float("nan"), torch.float64, lam))
 
     def cur(h, a, b, r, lam, c):
-        return tuple(masw.masw_curve(h, a, b, r, lam, c, flags=flags, team_warps=team_warps))
+        try:
+            return tuple(masw.masw_curve(h, a, b, r, lam, c, flags=flags, team_warps=team_warps))
+        except masw.MaswError as e:
+            L = lam.shape[0]
+            return (e.code, _filled((L,), float("nan"), torch.float64, lam),
+                    _filled((L,), -1, torch.int32, lam))
 
     def argmin(v):
         b, val = masw.masw_argmin(v)
@@ -106,25 +123,53 @@ def cuda_ops(flags: int = 0, team_warps: int = 0) -> Ops:
     return Ops(ens, cur, masw.masw_misfit, argmin)
 
 
+def _filled(shape, value, dtype, like):
+    return torch.full(shape, value, dtype=dtype, device=like.device)
+
+
+class ShardError(RuntimeError):
+    """A rank's shard failed (worst status over all ranks < 0); raised on every rank."""
+
+    def __init__(self, code: int, statuses):
+        self.code = int(code)
+        self.statuses = [int(x) for x in statuses]
+        super().__init__(f"sharded call failed: worst status {code} (per rank {self.statuses})")
+
+
+def worst_status(st: int, device, group=None) -> int:
+    """Worst status over ranks (errors negative, the warning positive); raises ShardError on
+    every rank if any rank failed."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    sts = [int(st)]
+    if world > 1:
+        t = torch.tensor([int(st)], dtype=torch.int64, device=device)
+        sts = _all_gather_padded(t, [1] * world, group).tolist()
+    lo, hi = min(sts), max(sts)
+    if lo < 0:
+        raise ShardError(lo, sts)
+    return hi
+
+
 # ------------------------------------------------------------------ collectives
 
 def _all_gather_padded(x: torch.Tensor, counts: Sequence[int], group=None) -> torch.Tensor:
-    """Concatenate per-rank first-dim blocks of unequal size (pad to the max, gather, trim)."""
+    """Concatenate per-rank first-dim blocks of unequal size (pad to the max, one
+    all_gather_into_tensor, trim).  The same collective on every backend (NCCL on the GPU
+    box, gloo in the CPU tests)."""
     world = len(counts)
     if world == 1:
         return x
     mx = max(counts)
-    pad = torch.zeros((mx,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-    pad[: x.shape[0]] = x
-    if dist.get_backend(group) == "nccl":
-        out = torch.empty((world * mx,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
-        dist.all_gather_into_tensor(out, pad, group=group)
-        parts = [out[k * mx: k * mx + counts[k]] for k in range(world)]
+    if x.shape[0] == mx:
+        pad = x.contiguous()
     else:
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad, group=group)
-        parts = [bufs[k][: counts[k]] for k in range(world)]
-    return torch.cat(parts, dim=0)
+        pad = torch.zeros((mx,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        pad[: x.shape[0]] = x
+    out = torch.empty((world * mx,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    if all(cnt == mx for cnt in counts):
+        return out
+    return torch.cat([out[k * mx: k * mx + counts[k]] for k in range(world)], dim=0)
 
 
 @dataclasses.dataclass
@@ -151,13 +196,16 @@ def ensemble_sharded(models_all, lam, c, ce, ops: Optional[Ops] = None, group=No
     M = h.shape[0]
     lo, hi = shard_bounds(M, world, rank)
     mv = lambda t: t[lo:hi].to(device) if device is not None else t[lo:hi]
-    st, ct, idx, mis = ops.curves_ensemble(mv(h), mv(a), mv(b), mv(r), lam, c, ce)
     counts = [shard_bounds(M, world, k)[1] - shard_bounds(M, world, k)[0] for k in range(world)]
-    st_t = torch.tensor([st], dtype=torch.int64, device=ct.device)
-    if world > 1:
-        # worst status: errors are negative, the warning positive -> gather and pick
-        sts = _all_gather_padded(st_t, [1] * world, group)
-        st = int(sts.min()) if int(sts.min()) < 0 else int(sts.max())
+    L = lam.shape[0]
+    if hi > lo:
+        st, ct, idx, mis = ops.curves_ensemble(mv(h), mv(a), mv(b), mv(r), lam, c, ce)
+    else:   # more ranks than models: an empty shard takes part in the collectives only
+        st, ct, idx, mis = (0, _filled((0, L), 0.0, torch.float64, lam),
+                            _filled((0, L), 0, torch.int32, lam),
+                            _filled((0,), 0.0, torch.float64, lam))
+    # worst status over ranks; every rank raises together if one failed
+    st = worst_status(st, ct.device, group)
     ct_all = _all_gather_padded(ct, counts, group)
     idx_all = _all_gather_padded(idx, counts, group)
     mis_all = _all_gather_padded(mis, counts, group)
@@ -181,11 +229,12 @@ def curve_sharded(model, lam: torch.Tensor, c, ce=None, strategy: str = "modular
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     W = lam.shape[0]
     mine, order, counts = partition_index(W, world, rank, strategy, lam.device)
-    st, ct, idx = ops.curve(*model, lam[mine], c)
-    if world > 1:
-        st_t = torch.tensor([st], dtype=torch.int64, device=ct.device)
-        sts = _all_gather_padded(st_t, [1] * world, group)
-        st = int(sts.min()) if int(sts.min()) < 0 else int(sts.max())
+    if counts[rank] > 0:
+        st, ct, idx = ops.curve(*model, lam[mine], c)
+    else:   # W < world: an empty shard takes part in the collectives only
+        st, ct, idx = (0, _filled((0,), 0.0, torch.float64, lam),
+                       _filled((0,), 0, torch.int32, lam))
+    st = worst_status(st, ct.device, group)
     ct_g = _all_gather_padded(ct, counts, group)
     idx_g = _all_gather_padded(idx, counts, group)
     order = order.to(ct_g.device)

@@ -27,6 +27,7 @@ SCHED_ROWS, SCHED_MODELS = 0x20, 0x40   # force the row / model-major scan kerne
 STABLE = 0x80   # cancellation-free, exponentially scaled element (f3), k h <= 700
 PIVOTED = 0x100   # every scan sign by the banded GEPP (validation / A-B)
 SCHED_PAIRS = 0x200   # force the pair scan (one model: two wavelengths per warp in lockstep)
+DIRECT = 0x400   # no small-c prefix: the direct element everywhere (reading S15''; A/B only)
 MAX_LAYERS = 64
 
 
@@ -88,6 +89,7 @@ def lib():
         L.masw_last_work.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
         L.masw_last_fallbacks.restype = ctypes.c_int64
         L.masw_last_fallbacks.argtypes = []
+        L.masw_last_prefix.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
         L.masw_probe_fp64_peak.argtypes = [ctypes.c_int32, ctypes.c_double,
                                            ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double)]
@@ -296,6 +298,14 @@ def masw_last_team_dets():
 def masw_last_fallbacks() -> int:
     """Determinants of the last synchronous scan re-evaluated with partial pivoting."""
     return int(lib().masw_last_fallbacks())
+
+
+def masw_last_prefix():
+    """(rows with a small-c prefix, dets evaluated there with the stable element) of the last
+    synchronous call (reading S15''); (-1, -1) if none was recorded."""
+    r, d = ctypes.c_int64(-1), ctypes.c_int64(-1)
+    lib().masw_last_prefix(ctypes.byref(r), ctypes.byref(d))
+    return int(r.value), int(d.value)
 
 
 def masw_last_work():

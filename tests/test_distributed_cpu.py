@@ -147,3 +147,58 @@ def test_gloo_world2_matches_single_process(orc):
         for strat, (gct, gidx, gmis, gst) in res.items():
             assert np.array_equal(gidx, cidx) and np.array_equal(gct, cct), strat
             assert gmis == cm and gst == st
+
+
+def _worker_failures(rank, world, port, q):
+    """Rank 1's model block holds an invalid model (beta > alpha): BOTH ranks must raise
+    ShardError after the status all-gather (none may hang in a collective); a curve with
+    fewer wavelengths than ranks leaves rank 1 an empty shard and still completes."""
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        ops = oracle_ops()
+        w = synth.workload("ensemble", M=6)
+        mods = w.models
+        t = lambda x: torch.from_numpy(np.ascontiguousarray(x))
+        beta = mods.beta.copy()
+        beta[5, 2] = 2.0 * mods.alpha[5, 2]          # model 5 lies in rank 1's block [3, 6)
+        raised = None
+        try:
+            D.ensemble_sharded((t(mods.h), t(mods.alpha), t(beta), t(mods.rho)), t(w.lam),
+                               t(w.c), t(w.ce), ops=ops)
+        except D.ShardError as e:
+            raised = (e.code, e.statuses)
+        c2 = synth.workload("maswaves")
+        m = c2.models
+        one = t(c2.lam[:1])
+        co = D.curve_sharded(tuple(t(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)), one,
+                             t(c2.c), None, ops=ops)
+        q.put((rank, raised, co.status, co.idx.numpy().copy(), co.ct.numpy().copy()))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover - surfaced through the queue
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+
+
+def test_gloo_world2_failure_raises_on_every_rank(orc):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_failures, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for o in outs:
+        assert o[1] != "error", o[2]
+    c2 = synth.workload("maswaves")
+    m = c2.models
+    st, cct, cidx, _ = orc.curve(m.h[0], m.alpha[0], m.beta[0], m.rho[0], c2.lam[:1], c2.c)
+    for rank, raised, cst, cidx_g, cct_g in outs:
+        assert raised is not None, f"rank {rank} did not raise"
+        code, sts = raised
+        assert code < 0 and sts[0] >= 0 and sts[1] == code      # rank 1 failed, rank 0 did not
+        assert cst == st and np.array_equal(cidx_g, cidx) and np.array_equal(cct_g, cct)

@@ -142,13 +142,13 @@ def test_stable_ensemble_matches_default_and_oracle(masw, orc):
 
 
 def test_small_c_false_change(masw, orc):
-    """Reading S15 at its extreme: a thin stiff lid (beta 491 m/s, 0.77 m) on a soft half-space
-    (beta 81 m/s) scanned from c = 0.5 m/s (c / beta_lid = 0.001, k h = 0.08).  50-digit
-    mpmath puts Re det K at +1.04e32 at c = 0.5, 1.0 and 1.5 m/s (no sign change there); the
-    direct App. A formulas cancel to ~u (beta / c)^4 / (k h)^4 relative error, so the default
-    scan's fp64 signs are unreliable at those first velocities (it reports a change at index 1
-    on this model; the fp64 oracle happens to keep the sign).  The stable element (f3,
-    MASW_STABLE) gets the true first change, as the oracle does."""
+    """Reading S15'' at its extreme: a thin stiff lid (beta 491 m/s, 0.77 m) on a soft
+    half-space (beta 81 m/s) scanned from c = 0.5 m/s (c / beta_lid = 0.001, k h = 0.08).
+    50-digit mpmath puts Re det K at +1.04e32 at c = 0.5, 1.0 and 1.5 m/s (no sign change
+    there); the direct App. A formulas' fp64 error scale there is P ~ 30, so their signs are
+    noise (MASW_DIRECT, the round-1 default, reports a false change at index 1).  The DEFAULT
+    path evaluates the small-c prefix with the stable element and returns the true first
+    change 161 -- in every scan -- as do MASW_STABLE and the oracle (binary128 there)."""
     import mpmath  # noqa: F401
 
     mods = synth.random_models(160, 1, 101)
@@ -158,9 +158,43 @@ def test_small_c_false_change(masw, orc):
     for cj in c[:3]:
         for l in lam:
             assert float(_mp_det(*a, float(l), float(cj), k_double=True).real) > 1e31
-    st, ct, idx = masw.masw_curve(*a, lam, c, flags=masw.STABLE)
     ost, oct_, oidx, _ = orc.curve(*a, lam, c)
-    assert st == ost == 0 and list(idx) == list(oidx) == [161, 161]
+    assert ost == 0 and list(oidx) == [161, 161]
+    for fl in (0, masw.SCHED_ROWS, masw.SCHED_PAIRS, masw.STABLE):
+        st, ct, idx = masw.masw_curve(*a, lam, c, flags=fl)
+        assert st == 0 and list(idx) == [161, 161], fl
+    # the same model inside an ensemble (model-major scan, forced)
+    M = np.repeat
+    ens = [np.ascontiguousarray(M(x[None], 8, axis=0)) for x in a]
+    r = masw.masw_curves_ensemble(*ens, lam, c, None, flags=masw.SCHED_MODELS)
+    assert r.status == 0 and np.all(np.asarray(r.idx) == 161)
+    rows, dets = masw.masw_last_prefix()
+    assert rows == 16 and dets > 0
+    # the direct element alone gets it wrong (the defect the prefix removes)
+    st, ct, idx = masw.masw_curve(*a, lam, c, flags=masw.DIRECT)
+    assert list(idx) != [161, 161]
+
+
+def test_prefix_holds_the_whole_curve(masw, orc):
+    """A 1 cm lid with a large P-wave velocity: Q_r reaches c* ~ 430 / 285 / 142 m/s at
+    lambda = 60 / 40 / 20 m, so for the first two every grid point up to the first change
+    (143.5 m/s) lies in the small-c prefix and the prefix kernel finds the change itself; for
+    the third the scan finds it right after the prefix.  A short grid entirely inside
+    the prefix without a change gives idx -1 (status WARN)."""
+    a = ([0.01], [3000.0, 1000.0], [200.0, 150.0], [1900.0, 2000.0])
+    lam = np.array([60.0, 40.0, 20.0])
+    c = 1.0 + 0.5 * np.arange(400, dtype=np.float64)
+    ost, oct_, oidx, _ = orc.curve(*a, lam, c)
+    for fl in (0, masw.SCHED_ROWS, masw.SCHED_PAIRS, masw.STABLE):
+        st, ct, idx = masw.masw_curve(*a, lam, c, flags=fl)
+        assert st == ost and np.array_equal(np.asarray(idx), oidx), fl
+    st, ct, idx = masw.masw_curve(*a, lam, c)
+    rows, dets = masw.masw_last_prefix()
+    assert rows == 3 and dets >= 2 * int(oidx[0] + 1)   # lambda = 60, 40: inside the prefix
+    short = c[:60]
+    ost, _, oidx2, _ = orc.curve(*a, lam, short)
+    st, ct, idx = masw.masw_curve(*a, lam, short)
+    assert st == ost == masw.WARN_NO_SIGN_CHANGE and list(idx) == list(oidx2) == [-1, -1, -1]
 
 
 def _dev(x):
