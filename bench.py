@@ -229,6 +229,12 @@ def run_ours(args):
     from paper_2003_02256_b200 import distributed as D
 
     rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N > 1 "
+                         "through torchrun, or let bench.py re-launch itself)")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} but only {torch.cuda.device_count()} "
+                         "visible CUDA device(s)")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -426,6 +432,7 @@ def run_ours(args):
     if not args.no_extra and world == 1:
         line["other_configs"] = other_configs(masw, torch, dev)
         line["other_configs"]["cold_vs_cached"] = cold_latency()
+        line["shard_projection"] = shard_projection(masw, torch, dev)
     if not args.no_cpu and world == 1:   # the oracle baseline runs at N = 1 only
         cores = host_cores()
         oidx = []
@@ -486,6 +493,62 @@ def uniform_scaling(masw, torch, dist, D, world, rank, dev, barrier, reps=3):
         ms, d = tt.tolist()
         out[mode] = {"wavelengths": L, "ms_per_curve": ms / reps, "dets_per_s": d / (ms / 1e3),
                      "curves_per_s": reps / (ms / 1e3)}
+    return out
+
+
+def shard_projection(masw, torch, dev, reps=5):
+    """PROJECTION (one GPU), not a scaling measurement: the device time of every rank's shard
+    at G = 1, 2, 4, 8 -- C5 models in contiguous blocks of 100k/G, C3 and C4 wavelengths
+    partitioned modularly, each shard timed alone on this GPU (CUDA events
+    around MASW_ASYNC calls, median of `reps`) -- and eff(G) = T(1) / (G * max_r T_r(G)), the
+    per-GPU efficiency the slowest rank would allow if the all-gather were free."""
+    from paper_2003_02256_b200 import distributed as D
+
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+
+    def timed(fn):
+        fn(0)                                        # validated, synchronous
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(masw.ASYNC)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    out = {"note": "projection from per-rank shards timed alone on one GPU; not a multi-GPU "
+                   "measurement (the all-gather is not included)"}
+    w = synth.workload("ensemble", M=100_000)
+    m = w.models
+    full = [t(x) for x in (m.h, m.alpha, m.beta, m.rho)]
+    lam, c, ce = t(w.lam), t(w.c), t(w.ce)
+    ens = {}
+    for G in (1, 2, 4, 8):
+        worst = 0.0
+        for r in range(G):
+            lo, hi = D.shard_bounds(100_000, G, r)
+            args = [x[lo:hi] for x in full]
+            worst = max(worst, timed(lambda fl: masw.masw_curves_ensemble(
+                *args, lam, c, ce, flags=fl)))
+        ens[G] = worst
+    out["ensemble_C5"] = {str(G): {"max_rank_ms": v, "eff": ens[1] / (G * v)} for G, v in ens.items()}
+    for key, name, kw in (("uniform_C3", "uniform", {"tier": 200.0}), ("realistic_C4", "realistic", {})):
+        w = synth.workload(name, **kw)
+        m = w.models
+        model = [t(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)]
+        c = t(w.c)
+        res = {}
+        for G in (1, 2, 4, 8):
+            worst = 0.0
+            for r in range(G):
+                lam_r = t(np.ascontiguousarray(w.lam[r::G]))
+                worst = max(worst, timed(lambda fl: masw.masw_curve(*model, lam_r, c, flags=fl)))
+            res[G] = worst
+        out[key] = {str(G): {"max_rank_ms": v, "eff": res[1] / (G * v)} for G, v in res.items()}
     return out
 
 
@@ -580,7 +643,24 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     return run_ours(args)
+
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` (N > 1) without a launcher: re-run this script under
+    torch.distributed.run with one process per GPU (rendezvous on 127.0.0.1), as the driver's
+    torchrun launch would."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

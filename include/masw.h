@@ -34,7 +34,7 @@
  *     The return code is the worst status: MASW_WARN_NO_SIGN_CHANGE (> 0) if any row is < 0.
  *
  * Validation (the same for every entry point that takes these arguments, in this order):
- *   MASW_E_ARG       null required pointer, L < 1, V < 2, V > INT32_MAX, M < 0,
+ *   MASW_E_ARG       null required pointer, L < 1, L > INT32_MAX, V < 2, V > INT32_MAX, M < 0,
  *                    N < 1 or N > MASW_MAX_LAYERS
  *   MASW_E_NONFINITE a NaN/Inf in lambda or c                                 (reading S9)
  *   MASW_E_GRID      lambda_i <= 0, c_0 <= 0, or c not strictly increasing

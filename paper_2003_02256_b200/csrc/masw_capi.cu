@@ -20,6 +20,7 @@
 #include "masw_internal.h"
 
 using namespace masw;
+static_assert(kMaxLayers == MASW_MAX_LAYERS, "masw_internal.h kMaxLayers");
 
 namespace {
 
@@ -29,6 +30,7 @@ thread_local Workspace *t_pinned_ws = nullptr;   // pinned host copy target for 
 // kScanRing launches, resolved lazily so MASW_ASYNC calls can be timed without host waits.
 constexpr int kScanRing = 64;
 thread_local cudaEvent_t t_scan_ev[kScanRing][2] = {};
+thread_local int t_scan_dev[kScanRing] = {};   // device + 1 the slot's events were created on
 thread_local long long t_scan_count = 0;   // TIME_SCAN launches recorded by this thread
 thread_local long long t_last_alg = -1, t_last_eval = -1, t_last_fb = -1;
 thread_local long long t_last_prefix_rows = -1, t_last_prefix_dets = -1;
@@ -221,7 +223,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
 {
     if (!mod_in.h || !mod_in.alpha || !mod_in.beta || !mod_in.rho || !lam || !c || !ct_out)
         return MASW_E_ARG;
-    if (L < 1 || V < 2 || V > INT32_MAX || mod_in.M < 0 || mod_in.N < 1 ||
+    if (L < 1 || L > INT32_MAX || V < 2 || V > INT32_MAX || mod_in.M < 0 || mod_in.N < 1 ||
         mod_in.N > MASW_MAX_LAYERS)
         return MASW_E_ARG;
     if (misfit_out && !ce) return MASW_E_ARG;
@@ -294,15 +296,30 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         const bool timed = (ex.flags & MASW_TIME_SCAN) != 0;
         cudaEvent_t *slot = t_scan_ev[t_scan_count % kScanRing];
         if (timed) {
-            if (!slot[0]) CK(cudaEventCreate(&slot[0]));
-            if (!slot[1]) CK(cudaEventCreate(&slot[1]));
+            // an event records only on a stream of its own device: (re)create the slot's pair
+            // on this call's device when the thread last used the slot on another one
+            int &sdev = t_scan_dev[t_scan_count % kScanRing];
+            if (sdev != dev + 1) {
+                for (int q = 0; q < 2; ++q)
+                    if (slot[q]) {
+                        cudaEventDestroy(slot[q]);
+                        slot[q] = nullptr;
+                    }
+                CK(cudaEventCreate(&slot[0]));
+                CK(cudaEventCreate(&slot[1]));
+                sdev = dev + 1;
+            }
             CK(cudaEventRecord(slot[0], st));
         }
         // reading S15'': the rows' small-c prefixes with the stable element, before the scan
         if (!stable && !(ex.flags & MASW_DIRECT)) {
             int32_t *pst = arena.alloc<int32_t>((size_t)R);
             int8_t *pca = arena.alloc<int8_t>((size_t)R);
-            CK(launch_smallc_prefix(sa, pst, pca, st, dev));
+            // per-model constants for the prefix pass (bounded: formed per element beyond)
+            const size_t lcb_bytes = (size_t)M * (size_t)(N + 1) * kLayerConstBytes;
+            void *lcb = (lcb_bytes <= (256u << 20)) ? arena.alloc<double2>(lcb_bytes / 16) : nullptr;
+            int64_t *plist = arena.alloc<int64_t>((size_t)R);
+            CK(launch_smallc_prefix(sa, pst, pca, plist, lcb, st, dev));
             sa.pstart = pst;
             sa.pcarry = pca;
         }

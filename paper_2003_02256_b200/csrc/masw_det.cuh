@@ -1246,7 +1246,10 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
 // by the caller with the banded GEPP (det_core), so the result always follows partial
 // pivoting where the unpivoted recursion is not certified.  (Reading S11: the values of
 // det K -- masw_det_grid, parity -- always come from the GEPP.)
-constexpr int kBlockMultExp = 12;   // multipliers up to 4096
+#ifndef MASW_BLOCK_MULT_EXP
+#define MASW_BLOCK_MULT_EXP 12
+#endif
+constexpr int kBlockMultExp = MASW_BLOCK_MULT_EXP;   // multipliers up to 4096 (variant builds: -D)
 
 struct SignOut {
     int sign;   // sgn(Re det K)

@@ -22,9 +22,14 @@ struct Workspace {
     int abort;                         // set by the scan kernel when validation failed
     int range_bad;                     // k_max * h_max > 350
     unsigned long long fallback_dets;  // sign re-evaluated with GEPP (block recursion not certified)
-    unsigned long long prefix_rows;    // rows with a small-c prefix (reading S15''; smallc_prefix_kernel)
+    unsigned long long prefix_rows;    // rows with a small-c prefix (reading S15''; smallc_rows_kernel)
     unsigned long long prefix_dets;    // determinants evaluated by smallc_prefix_kernel
 };
+
+// sizeof(LayerConst) (masw_det.cuh; static_assert in masw_kernels.cu) and MASW_MAX_LAYERS
+// (include/masw.h; static_assert in masw_capi.cu)
+constexpr size_t kLayerConstBytes = 48;
+constexpr int kMaxLayers = 64;
 
 // Model classes for Workspace::model_err
 constexpr unsigned kModelNonfinite = 1u;
@@ -82,11 +87,12 @@ cudaError_t launch_det_grid(const ModelArgs &m, const double *lam, int64_t L, co
                             int64_t V, double *mre, double *mim, int32_t *ex, Workspace *ws,
                             cudaStream_t st, bool stable = false, bool prefix = true);
 int auto_team_warps(int64_t rows, int64_t V, int device);
-// Reading S15'': evaluate every row's small-c prefix (grid points with c_j^4 < Q_r) with the
-// stable element, write pstart / pcarry (ScanArgs) and finish rows whose first change lies in
-// the prefix.  Runs before any scan kernel of the same call on the same stream.
-cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carry,
-                                 cudaStream_t st, int device);
+// Reading S15'': find and list the rows with a small-c prefix (grid points with c_j^4 < Q_r;
+// list: scratch for M L row ids; lcbuf: for M (N+1) k-free LayerConst, or nullptr), evaluate their prefixes with the stable element, write pstart /
+// pcarry (ScanArgs) and finish rows whose first change lies in the prefix.  Runs before any
+// scan kernel of the same call on the same stream.
+cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carry, int64_t *list,
+                                 void *lcbuf, cudaStream_t st, int device);
 // Model-major scan (ensembles): suitable when there are many (model, wavelength-block) items
 // and the per-warp caches fit two CTAs per SM; same outputs as launch_scan.
 bool models_scan_suitable(const ScanArgs &a, int device, bool forced);

@@ -173,16 +173,34 @@ __device__ __forceinline__ unsigned long long warp_sum_u64_pre(unsigned long lon
 constexpr double kSmallCTau = 1e-3;
 constexpr double kSmallCScale = 0x1p-53 / kSmallCTau;
 
-// Q_r of model m at wavenumber k (global-memory model arrays)
+// Q_r = s max_e (a_e + b_e / k^4) with a_e = 16 beta_e^4, b_e = (alpha_e beta_e / h_e^2)^2,
+// s = u / tau (e < N: the finite layers).  a_e, b_e depend on the model only; every user
+// (smallc_rows_kernel, det_grid_kernel) forms them and Q with these same operations, so the
+// prefix rule is bitwise the same everywhere.
+__device__ __forceinline__ void smallc_ab(double al, double be, double h, double &a, double &b)
+{
+    const double b2 = be * be;
+    a = (16.0 * b2) * b2;
+    const double t = (al * be) / (h * h);
+    b = t * t;
+}
+
+__device__ __forceinline__ double smallc_ik4(double k)
+{
+    const double kk = k * k;
+    return 1.0 / (kk * kk);
+}
+
+// Q_r of model m at wavenumber k (global-memory model arrays; det_grid_kernel)
 __device__ __forceinline__ double smallc_q(const ModelArgs &mod, int64_t m, double k)
 {
     const int N = mod.N;
+    const double ik4 = smallc_ik4(k);
     double worst = 0.0;
     for (int e = 0; e < N; ++e) {
-        const double al = mod.alpha[m * (N + 1) + e], be = mod.beta[m * (N + 1) + e];
-        const double kh = k * mod.h[m * N + e];
-        const double b2 = be * be, ab = al * be, kh2 = kh * kh;
-        worst = fmax(worst, fma(16.0 * b2, b2, (ab * ab) / (kh2 * kh2)));
+        double a, b;
+        smallc_ab(mod.alpha[m * (N + 1) + e], mod.beta[m * (N + 1) + e], mod.h[m * N + e], a, b);
+        worst = fmax(worst, fma(b, ik4, a));
     }
     return kSmallCScale * worst;
 }
@@ -208,26 +226,37 @@ __device__ __forceinline__ LayerConst row_layer_const(const ModelArgs &mod, int6
 
 // sgn Re det K (2: non-finite) of model m at (k, c') with the stable element: the certified
 // block recursion, the banded GEPP where it is not certified (or always, MASW_PIVOTED) --
-// what the row scan computes under MASW_STABLE.
+// what the row scan computes under MASW_STABLE.  lcm: the model's k-free LayerConst[N + 1]
+// (kh field = h; smallc_rows_kernel's cache, bitwise what row_layer_const forms), or nullptr
+// (formed from the model arrays per element).
 static __device__ __noinline__ int prefix_det_sign(ModelArgs mod, int64_t m, double k, double c,
-                                                   unsigned tab, bool pivoted)
+                                                   unsigned tab, bool pivoted,
+                                                   const LayerConst *lcm)
 {
     const int N = mod.N;
     const double c2 = c * c;
+    auto lc = [&](int e) {
+        if (lcm) {
+            LayerConst x = load_lc(lcm + e);
+            x.kh = (e < N) ? k * x.kh : 0.0;
+            return x;
+        }
+        return row_layer_const(mod, m, e, k);
+    };
     if (!pivoted) {
         const double ic2 = rcp_fast(c2);
         const SignOut so = det_sign_block_u<1>(
-            N, [&](int e) { return layer_elemu_stable(row_layer_const(mod, m, e, k), c2, ic2, tab); },
+            N, [&](int e) { return layer_elemu_stable(lc(e), c2, ic2, tab); },
             [&] {
-                const LayerConst H = row_layer_const(mod, m, N, k);
+                const LayerConst H = lc(N);
                 return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), H.aux * ic2);
             });
         if (so.ok) return so.sign;
     }
     const DetOut d = det_core<false, 0, 1>(
-        N, [&](int e) { return layer_elem_stable(row_layer_const(mod, m, e, k), c2, tab); },
+        N, [&](int e) { return layer_elem_stable(lc(e), c2, tab); },
         [&] {
-            const LayerConst H = row_layer_const(mod, m, N, k);
+            const LayerConst H = lc(N);
             return halfspace_k(halfspace_root(H.ia2, H.ib2, c2), lc_mu(H));
         });
     return d.bad ? 2 : d.sign;
@@ -249,53 +278,189 @@ __device__ __forceinline__ double perturb_model(const ModelArgs &mod, int64_t m,
 
 constexpr int kPrefixBlock = 256;
 
-__global__ void __launch_bounds__(kPrefixBlock) smallc_prefix_kernel(ScanArgs a, int32_t *pstart,
-                                                                     int8_t *pcarry)
+// Pass 1: a CTA takes a tile of kPrefixTile = 2048 consecutive output rows q = m L + i, a
+// thread 8 of them (strided by 256, so every store is coalesced and each thread has 8
+// independent chains in flight).  The per-layer terms a_e, b_e of Q_r (smallc_ab: one IEEE
+// division each) are formed once per (model, layer) of the tile in shared memory when they
+// fit (C5: ~52 models per tile), else per row.  n = #{j : c_j^4 < Q_r} (reading S15'') -- a
+// short linear probe, then bisection -- goes to pstart[q] (pass 2 replaces it) with
+// pcarry[q] = 0; ws->prefix_rows counts the rows with n > 0 (one reduction per CTA).  The CTA
+// also writes the k-free LayerConst[N + 1] of each model whose first row it holds to `lcbuf`
+// (if given) for pass 2.  (No validation check: on an invalid call the values are garbage
+// but every access stays in bounds, and pass 2 and the scans return without using them.)
+constexpr int kPrefixPerThread = 8;
+constexpr int kPrefixTile = kPrefixBlock * kPrefixPerThread;
+constexpr int kPrefixAbMax = 1024;   // (a_e, b_e) pairs staged per CTA (16 KB)
+
+__global__ void __launch_bounds__(kPrefixBlock) smallc_rows_kernel(ScanArgs a, int32_t *pstart,
+                                                                   int8_t *pcarry, int64_t *list,
+                                                                   LayerConst *lcbuf)
+{
+    __shared__ double2 s_ab[kPrefixAbMax];
+    __shared__ double s_ik4[kPrefixTile];
+    __shared__ unsigned s_off[kPrefixPerThread][kPrefixBlock / 32];
+    __shared__ unsigned long long s_base;
+    const int N = a.mod.N;
+    const int64_t M = a.mod.M, L = a.L, V = a.V, R = M * L;
+    const double *__restrict__ cg = a.c;
+    const int64_t q0 = (int64_t)blockIdx.x * kPrefixTile;
+    // the tile's models m_lo .. m_hi (q - m_lo L < kPrefixTile + L < 2^32: 32-bit divisions)
+    const int64_t m_lo = q0 / L;
+    const unsigned span = (unsigned)(min(q0 + kPrefixTile, R) - 1 - m_lo * L);
+    const unsigned nmod = span / (unsigned)L + 1u;
+    const bool staged = nmod * (unsigned)N <= (unsigned)kPrefixAbMax;
+    // 1/k^4 of the tile's wavelengths i_lo .. i_lo + ni - 1 (one model: a contiguous range;
+    // several: all L of them when L fits), else per row
+    const unsigned i_lo = (nmod == 1u) ? (unsigned)(q0 - m_lo * L) : 0u;
+    const unsigned ni = (nmod == 1u) ? span - i_lo + 1u : (L <= kPrefixTile ? (unsigned)L : 0u);
+    for (unsigned t = threadIdx.x; t < ni; t += kPrefixBlock)
+        s_ik4[t] = smallc_ik4(kTwoPi / a.lam[i_lo + t]);      // reading S2
+    if (staged) {
+        for (unsigned t = threadIdx.x; t < nmod * (unsigned)N; t += kPrefixBlock) {
+            const unsigned tm = t / (unsigned)N;
+            const int e = (int)(t - tm * (unsigned)N);
+            const int64_t mm = m_lo + tm;
+            double x, y;
+            smallc_ab(a.mod.alpha[mm * (N + 1) + e], a.mod.beta[mm * (N + 1) + e],
+                      a.mod.h[mm * N + e], x, y);
+            s_ab[t] = make_double2(x, y);
+        }
+    }
+    if (lcbuf) {   // models whose first row lies in this tile
+        for (unsigned t = threadIdx.x; t < nmod * (unsigned)(N + 1); t += kPrefixBlock) {
+            const unsigned tm = t / (unsigned)(N + 1);
+            const int e = (int)(t - tm * (unsigned)(N + 1));
+            const int64_t mm = m_lo + tm;
+            if (mm * L < q0) continue;
+            LayerConst x = row_layer_const(a.mod, mm, e, 1.0);
+            x.kh = (e < N) ? a.mod.h[mm * N + e] : 0.0;     // k-free: pass 2 forms k h
+            lcbuf[mm * (N + 1) + e] = x;
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned mk[kPrefixPerThread];   // per slab u: the warp's rows with n > 0
+#pragma unroll
+    for (int u = 0; u < kPrefixPerThread; ++u) {
+        const int64_t q = q0 + u * kPrefixBlock + threadIdx.x;
+        int n = 0;
+        if (q < R) {
+            const unsigned rq = (unsigned)(q - m_lo * L);
+            const unsigned dm = rq / (unsigned)L;
+            const int64_t m = m_lo + dm;
+            const unsigned i = rq - dm * (unsigned)L;
+            const double ik4 = ni ? s_ik4[i - i_lo] : smallc_ik4(kTwoPi / a.lam[i]);   // reading S2
+            double worst = 0.0;
+            if (staged) {
+                const double2 *ab = s_ab + dm * (unsigned)N;
+                for (int e = 0; e < N; ++e) worst = fmax(worst, fma(ab[e].y, ik4, ab[e].x));
+            } else {
+                for (int e = 0; e < N; ++e) {
+                    double x, y;
+                    smallc_ab(a.mod.alpha[m * (N + 1) + e], a.mod.beta[m * (N + 1) + e],
+                              a.mod.h[m * N + e], x, y);
+                    worst = fmax(worst, fma(y, ik4, x));
+                }
+            }
+            const double Q = kSmallCScale * worst;
+            auto below = [&](int64_t j) {
+                const double c2 = cg[j] * cg[j];
+                return c2 * c2 < Q;
+            };
+            if (below(0)) {                                       // first j with c_j^4 >= Q
+                int64_t lo = 1;
+                while (lo < V && lo < 8 && below(lo)) ++lo;      // prefixes are short (C5: 1-6)
+                if (lo == 8 && lo < V && below(lo)) {
+                    int64_t hi = V;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        if (below(mid)) lo = mid + 1; else hi = mid;
+                    }
+                }
+                n = (int)lo;
+            }
+            pstart[q] = n;
+            pcarry[q] = 0;
+        }
+        mk[u] = __ballot_sync(FULL, n > 0);
+        if (lane == 0) s_off[u][warp] = __popc(mk[u]);
+    }
+    // the tile's rows with n > 0 go to `list` in row order (u-major, then warp, then lane):
+    // one exclusive scan over the (u, warp) counts and one global atomic per CTA
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int u = 0; u < kPrefixPerThread; ++u)
+            for (int w = 0; w < kPrefixBlock / 32; ++w) {
+                const unsigned t = s_off[u][w];
+                s_off[u][w] = tot;
+                tot += t;
+            }
+        s_base = tot ? atomicAdd(&a.ws->prefix_rows, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPrefixPerThread; ++u)
+        if ((mk[u] >> lane) & 1u)
+            list[s_base + s_off[u][warp] + __popc(mk[u] & ((1u << lane) - 1u))] =
+                q0 + u * kPrefixBlock + threadIdx.x;
+}
+
+// Pass 2: the listed rows' prefix determinants with the stable element.  The prefixes are
+// short (C5: 1-6 grid points), so they are PACKED 32 to a warp pass: each warp takes 32 listed
+// rows, lays their prefix dets out contiguously and evaluates them in ceil(T / 32) passes
+// (C5: ~52 dets per 32 rows, 2 passes at ~80 % of the lanes) -- one row's 1-6 dets per warp
+// pass would idle 26-31 lanes.  Writes pstart (first index the scan evaluates, or -1 when the
+// row's first change lies in the prefix / the whole grid is prefix) and pcarry (the sign at
+// pstart - 1), and the outputs of the rows finished here.
+__global__ void __launch_bounds__(kPrefixBlock, 2) smallc_prefix_kernel(ScanArgs a, int32_t *pstart,
+                                                                        int8_t *pcarry,
+                                                                        const int64_t *list,
+                                                                        const LayerConst *lcbuf)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_abort;
     Workspace *ws = a.ws;
-    if (threadIdx.x == 0) s_abort = ws_invalid(ws, a.grid_mask, true);
+    if (threadIdx.x == 0) s_abort = ws_invalid(ws, a.grid_mask, true) || ws->prefix_rows == 0ull;
     __syncthreads();
     if (s_abort) return;
+    const int64_t nlist = (int64_t)ws->prefix_rows;
     exp_scale_fill(smem, ws_exp_rows(ws));
     __syncthreads();
     const unsigned ta = opaque(smem_addr(smem));
 
     const int lane = threadIdx.x & 31;
-    const int64_t M = a.mod.M, L = a.L, V = a.V, R = M * L;
+    const int64_t L = a.L, V = a.V;
     const double *__restrict__ cg = a.c;
     const int64_t nwarps = (int64_t)gridDim.x * (kPrefixBlock / 32);
-    unsigned long long my_alg = 0, my_eval = 0, my_rows = 0;
-    unsigned my_status = 0;
-    for (int64_t b = (int64_t)blockIdx.x * (kPrefixBlock / 32) + (threadIdx.x >> 5); b * 32 < R;
+    struct {
+        unsigned long long alg, eval;
+        unsigned status;
+    } acc{0ull, 0ull, 0u};
+    for (int64_t b = (int64_t)blockIdx.x * (kPrefixBlock / 32) + (threadIdx.x >> 5); b * 32 < nlist;
          b += nwarps) {
-        // ---- lane = one output row q = m L + i: its prefix length n = #{j : c_j^4 < Q}
-        const int64_t q = b * 32 + lane;
-        const bool valid = q < R;
-        const int64_t m = valid ? q / L : 0, i = valid ? q - m * L : 0;
-        const double k = kTwoPi / a.lam[i];                       // reading S2
-        int64_t n = 0;
-        if (valid) {
-            const double Q = smallc_q(a.mod, m, k);
-            int64_t lo = 0, hi = V;                               // first j with c_j^4 >= Q
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                const double c2 = cg[mid] * cg[mid];
-                if (c2 * c2 < Q) lo = mid + 1; else hi = mid;
-            }
-            n = lo;
+        const bool valid = b * 32 + lane < nlist;
+        const int64_t q = valid ? list[b * 32 + lane] : 0;
+        const int64_t n = valid ? (int64_t)pstart[q] : 0;
+        int64_t m, i;
+        if (q < 0x80000000ll && L < 0x80000000ll) {   // 32-bit division where it fits
+            const unsigned mq = (unsigned)q / (unsigned)L;
+            m = mq;
+            i = (int64_t)((unsigned)q - mq * (unsigned)L);
+        } else {
+            m = q / L;
+            i = q - m * L;
         }
-        // ---- pack the 32 rows' prefix dets: row o's dets are tasks excl_o .. excl_o + n_o - 1
+        const double k = kTwoPi / a.lam[i];                       // reading S2
+        // pack the rows' prefix dets: row o's dets are tasks excl_o .. excl_o + n_o - 1
         int64_t excl = n;
-#pragma unroll
+        #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int64_t t = __shfl_up_sync(FULL, excl, o);
             if (lane >= o) excl += t;
         }
         const int64_t T = __shfl_sync(FULL, excl, 31);
         excl -= n;
-        my_rows += (unsigned long long)__popc(__ballot_sync(FULL, n > 0));
         bool done = false, fbad = false;
         int64_t fj = -1;
         int prev = 0;   // sign of the previous task (across passes)
@@ -303,23 +468,25 @@ __global__ void __launch_bounds__(kPrefixBlock) smallc_prefix_kernel(ScanArgs a,
             const int64_t t = t0 + lane;
             const bool act = t < T;
             int o = 0;   // owner: the last lane with excl <= t (it has n > 0 when t < T)
-#pragma unroll
+        #pragma unroll
             for (int step = 16; step > 0; step >>= 1) {
                 const int64_t e = __shfl_sync(FULL, excl, o + step);
                 if (e <= t) o += step;
             }
             const int64_t jj = t - __shfl_sync(FULL, excl, o);
             const int64_t mo = __shfl_sync(FULL, m, o);
+            const int64_t qo = __shfl_sync(FULL, q, o);
             const double ko = __shfl_sync(FULL, k, o);
             const int64_t no = __shfl_sync(FULL, n, o);
             int s = 0;
             bool bad = false;
             if (act) {
                 const double cp = perturb_model(a.mod, mo, cg[jj]);
-                const int r = prefix_det_sign(a.mod, mo, ko, cp, ta, a.pivoted != 0);
+                const int r = prefix_det_sign(a.mod, mo, ko, cp, ta, a.pivoted != 0,
+                                              lcbuf ? lcbuf + mo * (a.mod.N + 1) : nullptr);
                 bad = (r == 2);
                 s = bad ? 0 : r;
-                if (jj == no - 1) pcarry[b * 32 + o] = (int8_t)s;   // the scan's carried sign
+                if (jj == no - 1) pcarry[qo] = (int8_t)s;   // the scan's carried sign
             }
             int sp = __shfl_up_sync(FULL, s, 1);
             if (lane == 0) sp = prev;
@@ -337,40 +504,37 @@ __global__ void __launch_bounds__(kPrefixBlock) smallc_prefix_kernel(ScanArgs a,
                 }
             }
         }
-        my_eval += (lane == 0) ? (unsigned long long)T : 0ull;
-        if (!valid) continue;
-        if (done) {                       // first change inside the prefix (Algorithm 1)
-            pstart[q] = -1;
-            if (fbad) {
+        acc.eval += (lane == 0) ? (unsigned long long)T : 0ull;
+        if (valid) {
+            if (done) {                       // first change inside the prefix (Algorithm 1)
+                pstart[q] = -1;
+                if (fbad) {
+                    a.ct[q] = __longlong_as_double(0x7ff8000000000000ll);
+                    if (a.idx) a.idx[q] = -2;
+                    acc.status |= 2u;
+                } else {
+                    a.ct[q] = cg[fj];
+                    if (a.idx) a.idx[q] = (int32_t)fj;
+                }
+                acc.alg += (unsigned long long)(fj + 1);
+            } else if (n >= V) {              // the whole grid was the prefix: no change
+                pstart[q] = -1;
                 a.ct[q] = __longlong_as_double(0x7ff8000000000000ll);
-                if (a.idx) a.idx[q] = -2;
-                my_status |= 2u;
-            } else {
-                a.ct[q] = cg[fj];
-                if (a.idx) a.idx[q] = (int32_t)fj;
-            }
-            my_alg += (unsigned long long)(fj + 1);
-        } else if (n >= V) {              // the whole grid was the prefix: no change
-            pstart[q] = -1;
-            a.ct[q] = __longlong_as_double(0x7ff8000000000000ll);
-            if (a.idx) a.idx[q] = -1;
-            my_status |= 1u;
-            my_alg += (unsigned long long)V;
-        } else {
-            pstart[q] = (int32_t)n;       // the scan starts here (carry written above)
-            if (n == 0) pcarry[q] = 0;
+                if (a.idx) a.idx[q] = -1;
+                acc.status |= 1u;
+                acc.alg += (unsigned long long)V;
+            }                                 // else: the scan starts at n (carry written above)
         }
     }
-    my_alg = warp_sum_u64_pre(my_alg);
-    my_eval = warp_sum_u64_pre(my_eval);
-    my_status = __reduce_or_sync(FULL, my_status);
+    const unsigned long long my_alg = warp_sum_u64_pre(acc.alg);
+    const unsigned long long my_eval = warp_sum_u64_pre(acc.eval);
+    const unsigned my_status = __reduce_or_sync(FULL, acc.status);
     if (lane == 0) {
         if (my_alg) atomicAdd(&ws->alg_dets, my_alg);
         if (my_eval) {
             atomicAdd(&ws->eval_dets, my_eval);
             atomicAdd(&ws->prefix_dets, my_eval);
         }
-        if (my_rows) atomicAdd(&ws->prefix_rows, my_rows);
         if (my_status) atomicOr(&ws->row_status, my_status);
     }
 }
@@ -1457,18 +1621,26 @@ size_t smem_optin_limit(int device)
 }
 }  // namespace
 
-cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carry,
-                                 cudaStream_t st, int device)
+cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carry, int64_t *list,
+                                 void *lcbuf, cudaStream_t st, int device)
 {
-    const size_t smem = kExpTabBytes;
-    cudaError_t e = ensure_smem_optin(smallc_prefix_kernel, device, 7);
-    if (e != cudaSuccess) return e;
     const int64_t rows = a.mod.M * a.L;
-    const int64_t need = (rows + kPrefixBlock - 1) / kPrefixBlock;   // 32 rows per warp
+    const int64_t blocks1 = (rows + kPrefixTile - 1) / kPrefixTile;
+    smallc_rows_kernel<<<(unsigned)blocks1, kPrefixBlock, 0, st>>>(
+        a, start, carry, list, static_cast<LayerConst *>(lcbuf));
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem = kExpTabBytes;
+    e = ensure_smem_optin(smallc_prefix_kernel, device, 7);
+    if (e != cudaSuccess) return e;
+    // at most all rows are listed (32 per warp); the kernel reads the actual count
     int64_t blocks = 2ll * sm_count(device);
+    const int64_t need = (rows + kPrefixBlock - 1) / kPrefixBlock;
     if (need < blocks) blocks = need;
     if (blocks < 1) blocks = 1;
-    smallc_prefix_kernel<<<(unsigned)blocks, kPrefixBlock, smem, st>>>(a, start, carry);
+    smallc_prefix_kernel<<<(unsigned)blocks, kPrefixBlock, smem, st>>>(
+        a, start, carry, list, static_cast<const LayerConst *>(lcbuf));
     count_launch();
     return cudaGetLastError();
 }

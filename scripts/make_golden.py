@@ -65,7 +65,39 @@ def main(which):
         print(f"c4: {time.time() - t:.1f}s, {int(nd.sum())} dets")
         write_curve("c4_ct_oracle.txt", f"C4 realistic N=5: oracle C_t, {int(nd.sum())} dets",
                     w.lam, idx, ct)
+    if "kappa" in which:
+        # reading S15': the kappa <= 1e-10 mask of the random det-parity sample of
+        # tests/test_gpu_parity.py::test_det_parity_random_ensemble_points (the long-double
+        # sensitivity analysis costs ~50 s per seed on 16 threads; the test recomputes the
+        # oracle's determinants live and re-checks a random subset of this mask)
+        w = synth.workload("ensemble", M=KAPPA_POOL)
+        for seed in (0, 1):
+            models, cs, masks = kappa_sample(w, seed)
+            kap = []
+            for mi, c in zip(models, cs):
+                a = tuple(x[mi] for x in (w.models.h, w.models.alpha, w.models.beta, w.models.rho))
+                kap.append(oracle.det_grid_kappa(*a, w.lam, c) <= KAPPA_MAX)
+            np.savez_compressed(os.path.join(OUT, f"kappa_mask_seed{seed}.npz"),
+                                models=np.asarray(models), c=np.asarray(cs),
+                                mask=np.packbits(np.asarray(kap)),
+                                shape=np.asarray(np.asarray(kap).shape),
+                                note=np.asarray("kappa <= 1e-10 (reading S15'), oracle.det_grid_kappa; "
+                                                "written by scripts/make_golden.py kappa"))
+
+
+# the random det-parity sample (tests/test_gpu_parity.py): KAPPA_MODELS of the first
+# KAPPA_POOL C5 models x C5's 40 lambda x KAPPA_C random c in [0.5 beta_min, 500]
+KAPPA_POOL, KAPPA_MODELS, KAPPA_C, KAPPA_MAX = 400, 20, 256, 1e-10
+
+
+def kappa_sample(w, seed):
+    rng = np.random.default_rng(seed)
+    models = [int(x) for x in rng.choice(KAPPA_POOL, KAPPA_MODELS, replace=False)]
+    cs = []
+    for mi in models:
+        cs.append(np.sort(rng.uniform(0.5 * w.models.beta[mi].min(), 500.0, KAPPA_C)))
+    return models, cs, None
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c2", "c3", "c4"])
+    main(sys.argv[1:] or ["c1", "c2", "c3", "c4", "kappa"])

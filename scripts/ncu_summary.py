@@ -69,8 +69,10 @@ def full(rep, out, dets=None):
             "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes": rd + wr,
             "fp64_pipe_pct_active": num(d, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
             "fp64_inst_pct_active": num(d, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
-            "issue_slots_busy_pct": num(d, "sm__instruction_throughput.avg.pct_of_peak_sustained_active")
-            or num(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            # issue utilisation = cycles in which the SMSP issued an instruction; NOT
+            # sm__instruction_throughput (a max-over-pipes roll-up, = the busiest pipe)
+            "issue_slots_busy_pct": num(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "instruction_throughput_pct": num(d, "sm__instruction_throughput.avg.pct_of_peak_sustained_active"),
             "alu_pipe_pct": num(d, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
             "fma_pipe_pct": num(d, "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
             "xu_pipe_pct": num(d, "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),

@@ -37,6 +37,11 @@ def margs(models, k=0):
 
 # ------------------------------------------------------------------ det grid parity (S15)
 
+# in-domain fractions measured from the oracle (scripts/det_domain_fractions.py ->
+# profiles/r2/det_domain.json); each floor sits just below its measured fraction
+DOMAIN_FLOOR = {"tiny": 0.95, "maswaves": 0.90, "maswaves_twin": 0.90}
+
+
 @pytest.mark.parametrize("name", ["tiny", "maswaves", "maswaves_twin"])
 def test_det_grid_parity(masw, orc, name):
     w = synth.workload(name)
@@ -48,7 +53,7 @@ def test_det_grid_parity(masw, orc, name):
     gm = gre + 1j * gim
     rel = parity.det_grid_rel_err(gm, gex, omant, oex)
     dom = parity.det_domain(omant, oex, w.c, w.models.beta.min(), kap)
-    assert dom.sum() > 0.3 * dom.size
+    assert dom.mean() > DOMAIN_FLOOR[name], dom.mean()   # measured 0.960 / 0.913 / 0.907
     worst = float(np.nanmax(rel[dom]))
     assert worst <= parity.DET_RTOL, worst
     # mantissa normalisation of the ABI (max(|re|,|im|) in [0.5, 1))
@@ -68,7 +73,7 @@ def test_det_grid_parity_uniform_n10(masw, orc):
     kap = orc.det_grid_kappa(*a, lam, c)
     rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
     dom = parity.det_domain(omant, oex, c, m.beta.min(), kap)
-    assert dom.mean() > 0.5
+    assert dom.mean() > 0.69, dom.mean()                 # measured 0.705
     assert float(np.nanmax(rel[dom])) <= parity.DET_RTOL
 
 
@@ -88,7 +93,7 @@ def test_det_grid_parity_thick_layers_whole_exp_range(masw, orc):
     kap = orc.det_grid_kappa(h, alpha, beta, rho, lam, c)
     rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
     dom = parity.det_domain(omant, oex, c, beta.min(), kap)
-    assert dom.mean() > 0.5
+    assert dom.mean() > 0.99, dom.mean()                 # measured 1.0
     assert float(np.nanmax(rel[dom])) <= parity.DET_RTOL
     with pytest.raises(masw.MaswError) as e:
         masw.masw_det_grid(np.array([0.7, 9.0, 55.8]), alpha, beta, rho, lam, c)
@@ -97,27 +102,40 @@ def test_det_grid_parity_thick_layers_whole_exp_range(masw, orc):
 
 @pytest.mark.parametrize("seed", [0, 1])
 def test_det_parity_random_ensemble_points(masw, orc, seed):
-    """Det parity on random C5 models at random (lambda, c): 16 models x 40 lambda x 96 c."""
+    """Det parity on random C5 models at random (lambda, c): 20 models x 40 lambda x 256 c
+    per seed (204,800 points).  The oracle's determinants are computed here; its kappa <= 1e-10
+    mask (reading S15', ~50 s of long-double sensitivity analysis per seed) comes from
+    tests/golden/kappa_mask_seed*.npz (scripts/make_golden.py kappa, oracle only), re-checked
+    here on a random subset of the points."""
     w = synth.workload("ensemble", M=400)
-    rng = np.random.default_rng(seed)
-    nm, nc = 16, 96
-    worst, n, where = 0.0, 0, None
-    for mi in rng.choice(400, nm, replace=False):
+    g = np.load(synth.GOLDEN_DIR + f"/kappa_mask_seed{seed}.npz")
+    models, cs = [int(x) for x in g["models"]], g["c"]
+    kmask = np.unpackbits(g["mask"])[: int(np.prod(g["shape"]))].reshape(tuple(g["shape"])) != 0
+    rng = np.random.default_rng(seed)                 # the sample the golden file was cut from
+    assert [int(x) for x in rng.choice(400, len(models), replace=False)] == models
+    chk = np.random.default_rng(100 + seed)
+    worst, n, tot, where = 0.0, 0, 0, None
+    for t, mi in enumerate(models):
         a = margs(w.models, mi)
-        c = np.sort(rng.uniform(0.5 * a[2].min(), 500.0, nc))
+        c = cs[t]
+        assert np.array_equal(c, np.sort(rng.uniform(0.5 * a[2].min(), 500.0, len(c))))
         gre, gim, gex = masw.masw_det_grid(*a, w.lam, c)
         st, omant, oex, _ = orc.det_grid(*a, w.lam, c)
-        kap = orc.det_grid_kappa(*a, w.lam, c)
+        # the cached mask is the oracle's kappa: re-derive 8 random points of this model
+        for _ in range(8):
+            i, j = int(chk.integers(len(w.lam))), int(chk.integers(len(c)))
+            assert (orc.det_kappa(*a, float(w.lam[i]), float(c[j])) <= parity.KAPPA_MAX) == kmask[t, i, j]
         rel = parity.det_grid_rel_err(gre + 1j * gim, gex, omant, oex)
-        dom = parity.det_domain(omant, oex, c, a[2].min(), kap)
+        dom = parity.det_domain(omant, oex, c, a[2].min(), None) & kmask[t]
         r = np.where(dom, rel, 0.0)
         k = np.unravel_index(np.argmax(r), r.shape)
         if r[k] > worst:
-            where = (int(mi), float(w.lam[k[0]]), float(c[k[1]]), float(kap[k]))
+            where = (int(mi), float(w.lam[k[0]]), float(c[k[1]]))
             worst = float(r[k])
         n += int(dom.sum())
-    assert n > 0.8 * nm * 40 * nc
-    # where = (model, lambda, c, kappa)
+        tot += dom.size
+    assert n > 0.95 * tot, n / tot                     # measured 0.969 / 0.962
+    # where = (model, lambda, c)
     assert worst <= parity.DET_RTOL, (worst, where)
 
 
@@ -495,6 +513,37 @@ def test_block_sign_vs_pivoted_ensemble(masw, orc):
                                               ia[m, i:i + 1], ib[m, i:i + 1])
         assert ok.all(), (m, i)
     assert 0 < fb < 1e-4 * ev, (fb, ev)
+
+
+def test_block_sign_vs_pivoted_random_models_1m(masw, orc):
+    """1,152,000 rows of random layered models (synth.random_models: reversals, stiff lids,
+    soft channels, Poisson ratios 0.18-0.46; N = 1..8, 6000 models each x 24 lambda) scanned
+    from the configs' 0.5 m/s grid start: the default sign (certified block recursion, GEPP
+    where uncertified, small-c prefix) against the all-GEPP scan (MASW_PIVOTED).  Every
+    differing row must be a near-root row the S16 rule allows (checked with the oracle); the
+    certificate's backward-error bound says a flip needs
+    K within ~2^15 u ||K|| of singular."""
+    lam = synth.geom(60.0, 0.8, 24)
+    c = 0.5 * (np.arange(1000, dtype=np.float64) + 1.0)
+    rows, differ, fb_tot, ev_tot = 0, 0, 0, 0
+    for N in range(1, 9):
+        mods = synth.random_models(6000, N, 700 + N)
+        args = [dev(x) for x in (mods.h, mods.alpha, mods.beta, mods.rho)] + [dev(lam), dev(c)]
+        a = masw.masw_curves_ensemble(*args, None)
+        fb_tot += masw.masw_last_fallbacks()
+        ev_tot += masw.masw_last_work()[1]
+        b = masw.masw_curves_ensemble(*args, None, flags=masw.PIVOTED)
+        assert a.status == b.status
+        ia, ib = a.idx.cpu().numpy(), b.idx.cpu().numpy()
+        rows += ia.size
+        for m, i in np.argwhere(ia != ib):
+            differ += 1
+            ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), lam[i:i + 1], c,
+                                                  ia[m, i:i + 1], ib[m, i:i + 1])
+            assert ok.all(), (N, int(m), int(i), int(ia[m, i]), int(ib[m, i]))
+    assert rows == 1_152_000
+    assert differ <= 1e-5 * rows, differ
+    assert 0 < fb_tot < 1e-3 * ev_tot, (fb_tot, ev_tot)
 
 
 def test_block_sign_vs_pivoted_single_curves(masw):

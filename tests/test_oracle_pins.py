@@ -6,6 +6,7 @@ term, a wrong sign or index, a transposed operand) fails at least one test.
 No GPU needed; marked ``not gpu`` implicitly.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -675,3 +676,23 @@ def test_ensemble_matches_per_model_curves_and_argmin(orc):
     assert out["misfit"][11] == out["misfit"][3]
     empty = orc.ensemble(mods.slice(0, 0), w.lam, w.c, w.ce)
     assert empty["status"] == 0 and empty["best"] == -1
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_kappa_mask_golden_is_the_oracles(orc, seed):
+    """tests/golden/kappa_mask_seed*.npz (the cached reading-S15' mask of the random det-parity
+    sample, scripts/make_golden.py kappa) equals oracle.det_kappa <= 1e-10 at 48 random points
+    and covers the sample the GPU test draws."""
+    import synth
+
+    g = np.load(os.path.join(synth.GOLDEN_DIR, f"kappa_mask_seed{seed}.npz"))
+    shape = tuple(int(x) for x in g["shape"])
+    mask = np.unpackbits(g["mask"])[: int(np.prod(shape))].reshape(shape) != 0
+    assert shape == (20, 40, 256) and 0.9 < mask.mean() < 1.0
+    w = synth.workload("ensemble", M=400)
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(48):
+        t, i, j = (int(rng.integers(n)) for n in shape)
+        mi = int(g["models"][t])
+        a = tuple(x[mi] for x in (w.models.h, w.models.alpha, w.models.beta, w.models.rho))
+        assert (orc.det_kappa(*a, float(w.lam[i]), float(g["c"][t][j])) <= 1e-10) == mask[t, i, j]
