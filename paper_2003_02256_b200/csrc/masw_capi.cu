@@ -326,7 +326,9 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
         if (models) {
             CK(launch_scan_models(sa, st, dev));
         } else if (pairs) {
-            CK(launch_scan_pairs(sa, st, dev));
+            const size_t tb = pair_tail_scratch_bytes(sa, dev);
+            void *tail = tb ? (void *)arena.alloc<double2>((tb + 15) / 16) : nullptr;
+            CK(launch_scan_pairs(sa, tail, st, dev));
         } else {
             CK(launch_scan(sa, team, st, dev));
         }

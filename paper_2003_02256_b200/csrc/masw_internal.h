@@ -65,6 +65,14 @@ struct ScanArgs {
     // nullptr: no prefix (MASW_STABLE / MASW_DIRECT), every row starts at 0.
     const int32_t *pstart;
     const int8_t *pcarry;
+    // pair scan only (set by its launcher): the last tail_pairs pair items are split into
+    // seg_count velocity segments of seg_len grid points each (tail segments);
+    // seg_found[2 tail_pairs]: each tail row's smallest in-segment event index (atomicMin);
+    // seg_rec[2 tail_pairs][seg_count]: per-segment record for pair_tail_combine_kernel
+    int64_t tail_pairs;
+    int seg_count, seg_len;
+    int *seg_found;
+    int2 *seg_rec;
 };
 
 // grid_mask bit: the call uses the stable element, range guard k h <= 700 instead of 350
@@ -98,7 +106,10 @@ cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carr
 bool models_scan_suitable(const ScanArgs &a, int device, bool forced);
 // pair scan (single curves of many wavelengths, two rows per warp in lockstep)
 bool pairs_scan_suitable(const ScanArgs &a, int device, bool forced);
-cudaError_t launch_scan_pairs(const ScanArgs &a, cudaStream_t st, int device,
+// Scratch bytes the pair scan needs for its tail segments (0: none); the caller passes that
+// many bytes (device, 16-byte aligned) to launch_scan_pairs.
+size_t pair_tail_scratch_bytes(const ScanArgs &a, int device);
+cudaError_t launch_scan_pairs(const ScanArgs &a, void *tail_scratch, cudaStream_t st, int device,
                               long long *warps_out = nullptr);
 long long scan_pairs_warps(const ScanArgs &a, int device);
 cudaError_t launch_scan_models(const ScanArgs &a, cudaStream_t st, int device,

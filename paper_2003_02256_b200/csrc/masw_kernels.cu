@@ -24,6 +24,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -1361,7 +1362,12 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
     const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;   // reading S15''
     const int64_t M = a.mod.M, L = a.L;
     const int64_t pairs_per_model = (L + 1) / 2;
-    const int64_t items = M * pairs_per_model;
+    // work items: the first Ph pair items whole, then the last Pt pair items as velocity
+    // segments, segment-major (all first segments, then all second segments, ...), so idle
+    // warps share the rows still running at the end instead of waiting on them
+    const int64_t P = M * pairs_per_model, Pt = a.tail_pairs, Ph = P - Pt;
+    const int S = a.seg_count, SEGV = a.seg_len;
+    const int64_t items = Ph + Pt * (int64_t)S;
     const int V = (int)a.V;
     const double *__restrict__ cg = a.c;
     const int nv = 2 * (N + 1);
@@ -1376,7 +1382,17 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
         if (lane == 0) item = (long long)atomicAdd(&ws->queue, 1ull);
         item = __shfl_sync(FULL, item, 0);
         if (item >= items) break;
-        const int64_t ip = item / M, m = item - ip * M;
+        int64_t pi = item, tp = -1;
+        int seg = -1, seg_lo = 0;
+        if (item >= Ph) {   // tail segment seg of tail pair tp
+            const int64_t t = item - Ph;
+            seg = (int)(t / Pt);
+            tp = t - (int64_t)seg * Pt;
+            pi = Ph + tp;
+            seg_lo = seg * SEGV;
+        }
+        const int seg_hi = (seg < 0) ? V : min(V, seg_lo + SEGV);
+        const int64_t ip = pi / M, m = pi - ip * M;
         const int64_t i0 = 2 * ip;
         const bool two = i0 + 1 < L;
         if (m != cur_m) {   // this model's k-free constants (as the model-major scan fills them)
@@ -1417,10 +1433,20 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
         }
         int carry0 = pc0, carry1 = pc1;
         bool pend0 = js0 >= 0, pend1 = two && js1 >= 0;
-        const int jlo = (pend0 && pend1) ? min(js0, js1) : (pend0 ? js0 : (pend1 ? js1 : 0));
-        for (int base = (jlo / 32) * 32; base < V && (pend0 || pend1); base += 32) {
+        if (seg >= 0) {   // rows with an event in an earlier segment need no more segments
+            if (pend0 && *(volatile int *)&a.seg_found[2 * tp] < seg_lo) pend0 = false;
+            if (pend1 && *(volatile int *)&a.seg_found[2 * tp + 1] < seg_lo) pend1 = false;
+        }
+        const bool rec0 = seg >= 0 && pend0, rec1 = seg >= 0 && pend1;   // write a record
+        int fs0 = 0, fs1 = 0;            // segment: sign at seg_lo
+        int ev0 = -1, ev1 = -1;          // segment: in-segment event index
+        bool eb0 = false, eb1 = false;   // segment: the event is a non-finite det
+        const int jlo = (seg >= 0) ? seg_lo
+                      : ((pend0 && pend1) ? min(js0, js1) : (pend0 ? js0 : (pend1 ? js1 : 0)));
+        const int jfirst = (seg >= 0) ? seg_lo : 0;   // no predecessor to compare with
+        for (int base = (jlo / 32) * 32; base < seg_hi && (pend0 || pend1); base += 32) {
             const int j = base + lane;
-            const bool valid = j < V;
+            const bool valid = j < seg_hi;
             double c = cg[valid ? j : V - 1];
             {   // reading S4, as in scan_kernel
                 const double clo = __shfl_sync(FULL, c, 0) - 1e-3;
@@ -1517,15 +1543,23 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                 s1 = pc1;
                 bad1 = false;
             }
-            // first-sign-change bookkeeping of one row for this chunk (as scan_kernel, TEAM 1)
-            auto settle = [&](long long r, int s, bool bad, int &carry, bool &pend) {
+            // first-sign-change bookkeeping of one row for this chunk (as scan_kernel, TEAM 1);
+            // a tail segment records its first sign / event instead of writing the row
+            auto settle = [&](long long r, int s, bool bad, int &carry, bool &pend, int &fs,
+                              int &evj, bool &evb, int tq) {
                 int sprev = __shfl_up_sync(FULL, s, 1);
                 if (lane == 0) sprev = carry;
-                const bool ev = valid && (bad || (j > 0 && s != sprev));
+                if (seg >= 0 && base == seg_lo) fs = __shfl_sync(FULL, s, 0);
+                const bool ev = valid && (bad || (j > jfirst && s != sprev));
                 const unsigned mask = __ballot_sync(FULL, ev);
                 if (mask) {
                     const int first = base + (__ffs(mask) - 1);
-                    if (j == first) {
+                    if (seg >= 0) {
+                        evj = first;
+                        evb = __shfl_sync(FULL, (int)bad, __ffs(mask) - 1) != 0;
+                        if (lane == 0) atomicMin(&a.seg_found[tq], first);
+                        team_alg += (unsigned long long)(first + 1 - seg_lo);
+                    } else if (j == first) {
                         if (bad) {
                             a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
                             if (a.idx) a.idx[r] = -2;
@@ -1536,13 +1570,27 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
                         }
                         my_alg += (unsigned long long)(j + 1);
                     }
-                    team_alg += (unsigned long long)(first + 1);
+                    if (seg < 0) team_alg += (unsigned long long)(first + 1);
                     pend = false;
                 }
-                carry = __shfl_sync(FULL, s, 31);
+                // the last valid lane's sign (the segment's last sign after its last chunk)
+                carry = __shfl_sync(FULL, s, min(31, seg_hi - 1 - base));
             };
-            if (pend0) settle(r0, s0, bad0, carry0, pend0);
-            if (pend1) settle(r0 + 1, s1, bad1, carry1, pend1);
+            if (pend0) settle(r0, s0, bad0, carry0, pend0, fs0, ev0, eb0, (int)(2 * tp));
+            if (pend1) settle(r0 + 1, s1, bad1, carry1, pend1, fs1, ev1, eb1, (int)(2 * tp + 1));
+        }
+        if (seg >= 0) {   // the segment's records: event index, first / last sign, flags
+            if (lane == 0) {
+                if (rec0)
+                    a.seg_rec[(2 * tp) * S + seg] =
+                        make_int2(ev0, (fs0 + 1) | ((carry0 + 1) << 2) | ((int)eb0 << 4) | 32);
+                if (rec1)
+                    a.seg_rec[(2 * tp + 1) * S + seg] =
+                        make_int2(ev1, (fs1 + 1) | ((carry1 + 1) << 2) | ((int)eb1 << 4) | 32);
+            }
+            team_alg += pend0 ? (unsigned long long)(seg_hi - seg_lo) : 0ull;   // no event
+            team_alg += pend1 ? (unsigned long long)(seg_hi - seg_lo) : 0ull;
+            continue;
         }
         for (int q = 0; q < 2; ++q) {
             const bool p = q ? pend1 : pend0;
@@ -1836,8 +1884,110 @@ bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
 }
 
 // Pair scan launcher: single curves (M == 1) of many wavelengths.  *warps_out: warps launched.
+// Combine the tail segments of each tail row (Algorithm 1 over the segment records in
+// velocity order): an event at a segment's first point is a non-finite det there or a sign
+// different from the previous segment's last sign; else the segment's in-segment event; else
+// carry its last sign on.  Writes C_t / idx and the work counters of the tail rows.
+__global__ void __launch_bounds__(256) pair_tail_combine_kernel(ScanArgs a)
+{
+    Workspace *ws = a.ws;
+    if (ws_invalid(ws, a.grid_mask, true)) return;
+    const int64_t M = a.mod.M, L = a.L, V = a.V;
+    const int64_t P = M * ((L + 1) / 2), Pt = a.tail_pairs, Ph = P - Pt;
+    const int S = a.seg_count, SEGV = a.seg_len;
+    const double *__restrict__ cg = a.c;
+    const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long alg = 0;
+    unsigned status = 0;
+    if (tq < 2 * Pt) {
+        const int64_t pi = Ph + tq / 2;
+        const int64_t ip = pi / M, m = pi - ip * M;
+        const int64_t i = 2 * ip + (tq & 1);
+        const int64_t r = m * L + i;
+        const bool live = i < L && !(a.pstart && a.pstart[r] < 0);   // else: none / prefix row
+        if (live) {
+            int carry = 0, evj = -1;
+            bool evb = false;
+            for (int sg = 0; sg < S && evj < 0; ++sg) {
+                const int lo = sg * SEGV;
+                if (lo >= V) break;
+                const int2 rec = a.seg_rec[tq * S + sg];
+                const int fs = (rec.y & 3) - 1, ls = ((rec.y >> 2) & 3) - 1;
+                const bool rb = (rec.y >> 4) & 1;
+                if (rec.x == lo) {                     // non-finite det at the first point
+                    evj = lo;
+                    evb = rb;
+                } else if (sg > 0 && fs != carry) {    // sign change across the boundary
+                    evj = lo;
+                } else if (rec.x > lo) {               // in-segment event
+                    evj = rec.x;
+                    evb = rb;
+                } else {
+                    carry = ls;
+                }
+            }
+            if (evj >= 0) {
+                if (evb) {
+                    a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                    if (a.idx) a.idx[r] = -2;
+                    status |= 2u;
+                } else {
+                    a.ct[r] = cg[evj];
+                    if (a.idx) a.idx[r] = evj;
+                }
+                alg = (unsigned long long)(evj + 1);
+            } else {
+                a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                if (a.idx) a.idx[r] = -1;
+                status |= 1u;
+                alg = (unsigned long long)V;
+            }
+        }
+    }
+    alg = warp_sum_u64(alg);
+    status = __reduce_or_sync(FULL, status);
+    if ((threadIdx.x & 31) == 0) {
+        if (alg) atomicAdd(&ws->alg_dets, alg);
+        if (status) atomicOr(&ws->row_status, status);
+    }
+}
+
+// Tail segments of the pair scan: the pair items of the last (partial) round -- all of them
+// when there are fewer pairs than warps -- are split into velocity segments (a multiple of 32
+// grid points each), about 8 per warp in total.
+struct PairTail {
+    int64_t pairs;
+    int count, len;
+};
+
+static PairTail pair_tail_plan(const ScanArgs &a, int64_t warps)
+{
+    PairTail t{0, 0, 0};
+    const int64_t P = a.mod.M * ((a.L + 1) / 2);
+    if (warps < 2 || a.V < 64) return t;
+    // tail = the pairs of the last, partial round (P mod warps; all pairs when P <= warps),
+    // in about 8 segments per warp.  Measured on C3 (profiles/r2/pair_tail_sweep.txt, same box): no
+    // tail 6.14 ms; partial round 5.23 ms (4 segments per warp: 5.29, 16: 5.21); half a round
+    // of warps: 5.38-5.94; a full round: 5.44-6.44 (more speculative segments past the
+    // change).  C4 (lengths sorted longest first): 1.75 -> 1.71-1.74 ms either way.
+    constexpr double kPerWarp = 8.0;
+    int64_t Pt = P % warps;
+    if (P <= warps) Pt = P;
+    if (Pt < 1) return t;
+    const int64_t chunks = (a.V + 31) / 32;
+    int64_t S = (int64_t)((kPerWarp * (double)warps + (double)Pt - 1) / (double)Pt);
+    S = std::max<int64_t>(1, std::min<int64_t>(S, chunks));
+    if (S < 2) return t;   // no split: whole pairs
+    const int64_t len = ((chunks + S - 1) / S) * 32;
+    t.pairs = Pt;
+    t.len = (int)len;
+    t.count = (int)((a.V + len - 1) / len);
+    return t;
+}
+
 static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
-                                long long *warps_out, bool dry)
+                                long long *warps_out, bool dry, void *scratch = nullptr,
+                                size_t *scratch_bytes = nullptr)
 {
     const size_t smem = pair_smem_bytes(a.mod.N);
     auto kern = a.stable ? scan_pair_kernel<true> : scan_pair_kernel<false>;
@@ -1863,13 +2013,41 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
     }
     if (per_sm < 0) return cudaErrorInvalidConfiguration;
     const int wpc = kPairBlock / 32;
-    int64_t blocks = (int64_t)sms * per_sm;
-    const int64_t need = (a.mod.M * ((a.L + 1) / 2) + wpc - 1) / wpc;
+    const int64_t full = (int64_t)sms * per_sm;
+    const PairTail tail = pair_tail_plan(a, full * wpc);
+    const int64_t P = a.mod.M * ((a.L + 1) / 2);
+    const int64_t items = P - tail.pairs + tail.pairs * tail.count;
+    int64_t blocks = full;
+    const int64_t need = (items + wpc - 1) / wpc;
     if (need < blocks) blocks = need;
     if (blocks < 1) blocks = 1;
     if (warps_out) *warps_out = blocks * wpc;
+    const size_t found_bytes = (size_t)(2 * tail.pairs) * sizeof(int);
+    const size_t rec_off = (found_bytes + 15) & ~(size_t)15;
+    const size_t need_bytes = tail.pairs ? rec_off + (size_t)(2 * tail.pairs) * tail.count * sizeof(int2)
+                                         : 0;
+    if (scratch_bytes) *scratch_bytes = need_bytes;
     if (dry) return cudaSuccess;
-    kern<<<(unsigned)blocks, kPairBlock, smem, st>>>(a);
+    ScanArgs b = a;
+    b.tail_pairs = 0;
+    b.seg_count = 0;
+    b.seg_len = 0;
+    b.seg_found = nullptr;
+    b.seg_rec = nullptr;
+    if (tail.pairs && scratch) {
+        b.tail_pairs = tail.pairs;
+        b.seg_count = tail.count;
+        b.seg_len = tail.len;
+        b.seg_found = static_cast<int *>(scratch);
+        b.seg_rec = reinterpret_cast<int2 *>(static_cast<unsigned char *>(scratch) + rec_off);
+        cudaError_t e = cudaMemsetAsync(b.seg_found, 0x7f, found_bytes, st);   // "no event yet"
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<(unsigned)blocks, kPairBlock, smem, st>>>(b);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !b.tail_pairs) return e;
+    pair_tail_combine_kernel<<<(unsigned)((2 * b.tail_pairs + 255) / 256), 256, 0, st>>>(b);
     count_launch();
     return cudaGetLastError();
 }
@@ -1884,9 +2062,18 @@ bool pairs_scan_suitable(const ScanArgs &a, int device, bool forced)
     return launch_pairs(a, nullptr, device, &w, true) == cudaSuccess;
 }
 
-cudaError_t launch_scan_pairs(const ScanArgs &a, cudaStream_t st, int device, long long *warps_out)
+size_t pair_tail_scratch_bytes(const ScanArgs &a, int device)
 {
-    return launch_pairs(a, st, device, warps_out, false);
+    size_t bytes = 0;
+    long long w = 0;
+    if (launch_pairs(a, nullptr, device, &w, true, nullptr, &bytes) != cudaSuccess) return 0;
+    return bytes;
+}
+
+cudaError_t launch_scan_pairs(const ScanArgs &a, void *tail_scratch, cudaStream_t st, int device,
+                              long long *warps_out)
+{
+    return launch_pairs(a, st, device, warps_out, false, tail_scratch);
 }
 
 long long scan_pairs_warps(const ScanArgs &a, int device)
