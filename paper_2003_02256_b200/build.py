@@ -41,6 +41,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     if out is None and not force and not stale():
         return LIB
     objdir = os.path.join(PKG, "build")
+    if out is not None:   # variant builds: their own objects (parallel builds do not collide)
+        objdir = os.path.join(objdir, os.path.basename(out).replace(".", "_"))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for s in SOURCES:

@@ -279,9 +279,10 @@ __device__ __forceinline__ double perturb_model(const ModelArgs &mod, int64_t m,
 
 constexpr int kPrefixBlock = 256;
 
-// Pass 1: a CTA takes a tile of kPrefixTile = 2048 consecutive output rows q = m L + i, a
-// thread 8 of them (strided by 256, so every store is coalesced and each thread has 8
-// independent chains in flight).  The per-layer terms a_e, b_e of Q_r (smallc_ab: one IEEE
+// Pass 1: a CTA takes a tile of 256 PER consecutive output rows q = m L + i, a thread PER of
+// them (strided by 256, so every store is coalesced and each thread has PER independent
+// chains in flight; PER = 8 for large calls, 1 when that leaves the GPU short of CTAs -- a
+// single 10k-wavelength curve ran in 5 CTAs of 8-row threads, 30 us under ncu).  The per-layer terms a_e, b_e of Q_r (smallc_ab: one IEEE
 // division each) are formed once per (model, layer) of the tile in shared memory when they
 // fit (C5: ~52 models per tile), else per row.  n = #{j : c_j^4 < Q_r} (reading S15'') -- a
 // short linear probe, then bisection -- goes to pstart[q] (pass 2 replaces it) with
@@ -289,17 +290,18 @@ constexpr int kPrefixBlock = 256;
 // also writes the k-free LayerConst[N + 1] of each model whose first row it holds to `lcbuf`
 // (if given) for pass 2.  (No validation check: on an invalid call the values are garbage
 // but every access stays in bounds, and pass 2 and the scans return without using them.)
-constexpr int kPrefixPerThread = 8;
-constexpr int kPrefixTile = kPrefixBlock * kPrefixPerThread;
+constexpr int kPrefixPerThread = 8;   // PER of large calls
 constexpr int kPrefixAbMax = 1024;   // (a_e, b_e) pairs staged per CTA (16 KB)
 
+template <int PER>
 __global__ void __launch_bounds__(kPrefixBlock) smallc_rows_kernel(ScanArgs a, int32_t *pstart,
                                                                    int8_t *pcarry, int64_t *list,
                                                                    LayerConst *lcbuf)
 {
     __shared__ double2 s_ab[kPrefixAbMax];
+    constexpr int kPrefixTile = kPrefixBlock * PER;
     __shared__ double s_ik4[kPrefixTile];
-    __shared__ unsigned s_off[kPrefixPerThread][kPrefixBlock / 32];
+    __shared__ unsigned s_off[PER][kPrefixBlock / 32];
     __shared__ unsigned long long s_base;
     const int N = a.mod.N;
     const int64_t M = a.mod.M, L = a.L, V = a.V, R = M * L;
@@ -340,9 +342,9 @@ __global__ void __launch_bounds__(kPrefixBlock) smallc_rows_kernel(ScanArgs a, i
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned mk[kPrefixPerThread];   // per slab u: the warp's rows with n > 0
+    unsigned mk[PER];   // per slab u: the warp's rows with n > 0
 #pragma unroll
-    for (int u = 0; u < kPrefixPerThread; ++u) {
+    for (int u = 0; u < PER; ++u) {
         const int64_t q = q0 + u * kPrefixBlock + threadIdx.x;
         int n = 0;
         if (q < R) {
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(kPrefixBlock) smallc_rows_kernel(ScanArgs a, i
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned tot = 0;
-        for (int u = 0; u < kPrefixPerThread; ++u)
+        for (int u = 0; u < PER; ++u)
             for (int w = 0; w < kPrefixBlock / 32; ++w) {
                 const unsigned t = s_off[u][w];
                 s_off[u][w] = tot;
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(kPrefixBlock) smallc_rows_kernel(ScanArgs a, i
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < kPrefixPerThread; ++u)
+    for (int u = 0; u < PER; ++u)
         if ((mk[u] >> lane) & 1u)
             list[s_base + s_off[u][warp] + __popc(mk[u] & ((1u << lane) - 1u))] =
                 q0 + u * kPrefixBlock + threadIdx.x;
@@ -1673,9 +1675,14 @@ cudaError_t launch_smallc_prefix(const ScanArgs &a, int32_t *start, int8_t *carr
                                  void *lcbuf, cudaStream_t st, int device)
 {
     const int64_t rows = a.mod.M * a.L;
-    const int64_t blocks1 = (rows + kPrefixTile - 1) / kPrefixTile;
-    smallc_rows_kernel<<<(unsigned)blocks1, kPrefixBlock, 0, st>>>(
-        a, start, carry, list, static_cast<LayerConst *>(lcbuf));
+    constexpr int64_t kBig = (int64_t)kPrefixBlock * kPrefixPerThread;
+    if (rows >= 2ll * sm_count(device) * kBig) {
+        smallc_rows_kernel<kPrefixPerThread><<<(unsigned)((rows + kBig - 1) / kBig), kPrefixBlock, 0, st>>>(
+            a, start, carry, list, static_cast<LayerConst *>(lcbuf));
+    } else {
+        smallc_rows_kernel<1><<<(unsigned)((rows + kPrefixBlock - 1) / kPrefixBlock), kPrefixBlock, 0, st>>>(
+            a, start, carry, list, static_cast<LayerConst *>(lcbuf));
+    }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1885,10 +1892,13 @@ bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
 
 // Pair scan launcher: single curves (M == 1) of many wavelengths.  *warps_out: warps launched.
 // Combine the tail segments of each tail row (Algorithm 1 over the segment records in
-// velocity order): an event at a segment's first point is a non-finite det there or a sign
-// different from the previous segment's last sign; else the segment's in-segment event; else
-// carry its last sign on.  Writes C_t / idx and the work counters of the tail rows.
-__global__ void __launch_bounds__(256) pair_tail_combine_kernel(ScanArgs a)
+// velocity order), one warp per row, 32 segments per step: segment sg holds the row's first
+// event iff it is the first segment with an event -- a non-finite det at its first point, a
+// first sign different from the previous segment's last sign, or an in-segment event (the
+// segments before the first event were all written: a segment is skipped only after an
+// earlier one found an event).  Writes C_t / idx and the work counters of the tail rows.
+constexpr int kCombineBlock = 256;
+__global__ void __launch_bounds__(kCombineBlock) pair_tail_combine_kernel(ScanArgs a)
 {
     Workspace *ws = a.ws;
     if (ws_invalid(ws, a.grid_mask, true)) return;
@@ -1896,7 +1906,8 @@ __global__ void __launch_bounds__(256) pair_tail_combine_kernel(ScanArgs a)
     const int64_t P = M * ((L + 1) / 2), Pt = a.tail_pairs, Ph = P - Pt;
     const int S = a.seg_count, SEGV = a.seg_len;
     const double *__restrict__ cg = a.c;
-    const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t tq = ((int64_t)blockIdx.x * kCombineBlock + threadIdx.x) >> 5;   // warp: row
     unsigned long long alg = 0;
     unsigned status = 0;
     if (tq < 2 * Pt) {
@@ -1906,47 +1917,66 @@ __global__ void __launch_bounds__(256) pair_tail_combine_kernel(ScanArgs a)
         const int64_t r = m * L + i;
         const bool live = i < L && !(a.pstart && a.pstart[r] < 0);   // else: none / prefix row
         if (live) {
-            int carry = 0, evj = -1;
+            int evj = -1;
             bool evb = false;
-            for (int sg = 0; sg < S && evj < 0; ++sg) {
+            int prev_ls = 0;   // the last sign of the segment before this step's first one
+            for (int s0 = 0; s0 < S && s0 * SEGV < V; s0 += 32) {
+                const int sg = s0 + lane;
                 const int lo = sg * SEGV;
-                if (lo >= V) break;
-                const int2 rec = a.seg_rec[tq * S + sg];
+                const bool in = sg < S && lo < V;
+                const int2 rec = in ? a.seg_rec[tq * S + sg] : make_int2(-1, 0);
                 const int fs = (rec.y & 3) - 1, ls = ((rec.y >> 2) & 3) - 1;
+                int pls = __shfl_up_sync(FULL, ls, 1);
+                if (lane == 0) pls = prev_ls;
+                // this segment's event, in the precedence of Algorithm 1 over its points: a
+                // non-finite det at the first point, a change across the boundary, an
+                // in-segment event (rec.x: -1 or in [lo, lo + SEGV))
                 const bool rb = (rec.y >> 4) & 1;
-                if (rec.x == lo) {                     // non-finite det at the first point
-                    evj = lo;
-                    evb = rb;
-                } else if (sg > 0 && fs != carry) {    // sign change across the boundary
-                    evj = lo;
-                } else if (rec.x > lo) {               // in-segment event
-                    evj = rec.x;
-                    evb = rb;
-                } else {
-                    carry = ls;
+                int cj = -1;
+                bool cb = false;
+                if (in) {
+                    if (rec.x == lo) {
+                        cj = lo;
+                        cb = rb;
+                    } else if (sg > 0 && fs != pls) {
+                        cj = lo;
+                    } else if (rec.x > lo) {
+                        cj = rec.x;
+                        cb = rb;
+                    }
                 }
+                const unsigned mk = __ballot_sync(FULL, cj >= 0);
+                if (mk) {
+                    const int src = __ffs(mk) - 1;
+                    evj = __shfl_sync(FULL, cj, src);
+                    evb = __shfl_sync(FULL, (int)cb, src) != 0;
+                    break;
+                }
+                prev_ls = __shfl_sync(FULL, ls, 31);
             }
-            if (evj >= 0) {
-                if (evb) {
-                    a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
-                    if (a.idx) a.idx[r] = -2;
-                    status |= 2u;
+            if (lane == 0) {
+                if (evj >= 0) {
+                    if (evb) {
+                        a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                        if (a.idx) a.idx[r] = -2;
+                        status |= 2u;
+                    } else {
+                        a.ct[r] = cg[evj];
+                        if (a.idx) a.idx[r] = evj;
+                    }
+                    alg = (unsigned long long)(evj + 1);
                 } else {
-                    a.ct[r] = cg[evj];
-                    if (a.idx) a.idx[r] = evj;
+                    a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                    if (a.idx) a.idx[r] = -1;
+                    status |= 1u;
+                    alg = (unsigned long long)V;
                 }
-                alg = (unsigned long long)(evj + 1);
-            } else {
-                a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
-                if (a.idx) a.idx[r] = -1;
-                status |= 1u;
-                alg = (unsigned long long)V;
             }
         }
     }
     alg = warp_sum_u64(alg);
     status = __reduce_or_sync(FULL, status);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         if (alg) atomicAdd(&ws->alg_dets, alg);
         if (status) atomicOr(&ws->row_status, status);
     }
@@ -2047,7 +2077,8 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !b.tail_pairs) return e;
-    pair_tail_combine_kernel<<<(unsigned)((2 * b.tail_pairs + 255) / 256), 256, 0, st>>>(b);
+    pair_tail_combine_kernel<<<(unsigned)((2 * b.tail_pairs * 32 + kCombineBlock - 1) / kCombineBlock),
+                               kCombineBlock, 0, st>>>(b);
     count_launch();
     return cudaGetLastError();
 }
