@@ -1,24 +1,24 @@
-"""batched dense-LU baseline on B200.
+"""batched dense-LU baseline on B200 at throughput scale.
 
 The paper's first GPU pipeline: assemble every dense complex stiffness matrix of the
-(lambda, c) grid in global memory (one matrix per (lambda, c), 2(N+1)^2 x 16 B), then a
-batched complex LU (cublasZgetrfBatched; here torch.linalg.det -> cuSOLVER/cuBLAS batched
-getrf) and the sign search.  This script times that pipeline against libmasw's banded
-kernels on the same grids and checks that both give the same C_t:
+(lambda, c) grid in global memory (one 2(N+1) x 2(N+1) complex matrix per point), then a
+batched complex LU (cublasZgetrfBatched on the K620; here torch.linalg.det, i.e. the vendor
+batched getrf) and the sign search.  This script times that pipeline against libmasw on the
+same full grids, >= 1e7 determinants per side, the dense side in chunks of 2^20 matrices
+(2.4 GB at N = 5, 7.7 GB at N = 10):
 
-  * full det grid, no early exit (the paper's GPU computed "all stiffness matrices
-    regardless"): dense assemble + batched LU  vs  masw_det_grid;
-  * C_t of whole curves: dense grid + first-sign-change search  vs  masw_curve /
-    masw_curves_ensemble (early exit).
-
-The dense assembly is vectorised torch complex128 arithmetic on the GPU, written from the
-same formulas; it is a comparison arm, not part of the product.
+  * dense assembly (vectorised torch complex128, written from SURVEY.md App. A -- a
+    comparison arm, not part of the product), the batched LU alone, and both;
+  * masw_det_grid: every det K on the grid (values, banded GEPP, no early exit -- the paper's
+    banded kernel also computed every determinant);
+  * masw_curve: the product path (early exit, algorithmic dets/s) for context;
+  * sign agreement of Re det between the dense LU and the banded values over the whole grid
+    (the oracle check of both on a sample is tests/test_gpu_f2.py).
 
     python scripts/dense_lu_baseline.py [out.json]
 """
 import json
 import os
-import statistics
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -28,14 +28,14 @@ import torch  # noqa: E402
 import paper_2003_02256_b200 as masw  # noqa: E402
 import synth  # noqa: E402
 
-dev = torch.device("cuda:0")
 TWO_PI = 6.283185307179586
+CHUNK = 1 << 20
 
 
 def perturb(c, alpha, beta):
-    """Reading S4 on a tensor of velocities (up to 4 rounds, enough for the grids here)."""
+    """Reading S4 for one model on a tensor of velocities."""
     vel = torch.cat([alpha, beta])
-    for _ in range(4):
+    for _ in range(16):
         near = (torch.abs(c[..., None] - vel) < 1e-4).any(-1)
         if not bool(near.any()):
             break
@@ -43,102 +43,133 @@ def perturb(c, alpha, beta):
     return c
 
 
-def dense_K(h, alpha, beta, rho, lam, c):
-    """Dense complex K for every (lambda_i, c_j): [L, V, n, n] complex128."""
+def dense_K(h, alpha, beta, rho, k, cp):
+    """Dense complex K at the points (k[b], cp[b]) (cp: S4-perturbed): [B, n, n] complex128.
+
+    One model: h [N], alpha/beta/rho [N+1] (float64 tensors); k, cp [B] float64."""
     N = h.shape[0]
     n = 2 * (N + 1)
-    k = (TWO_PI / lam)[:, None].to(torch.complex128)                    # [L,1]
-    cp = perturb(c, alpha, beta)[None, :].to(torch.complex128)         # [1,V]
-    L, V = lam.shape[0], c.shape[0]
-    K = torch.zeros((L, V, n, n), dtype=torch.complex128, device=c.device)
+    B = k.shape[0]
+    kc = k.to(torch.complex128)
+    c2 = (cp * cp).to(torch.complex128)
+    K = torch.zeros((B, n, n), dtype=torch.complex128, device=k.device)
     for e in range(N + 1):
-        al, be, rh = alpha[e].item(), beta[e].item(), rho[e].item()
-        r = torch.sqrt(1.0 - cp * cp / (al * al))
-        s = torch.sqrt(1.0 - cp * cp / (be * be))
-        if e == N:
-            mu = k * rh * be * be
+        al, be, rh = float(alpha[e]), float(beta[e]), float(rho[e])
+        r = torch.sqrt(1.0 - c2 / (al * al))          # principal branch (reading S3)
+        s = torch.sqrt(1.0 - c2 / (be * be))
+        if e == N:                                     # half-space (App. A)
+            mu = kc * (rh * be * be)
             q = (1.0 - s * s) / (1.0 - r * s)
-            K[..., 2 * N, 2 * N] += (mu * r * q)
-            K[..., 2 * N, 2 * N + 1] += (mu * q - 2.0 * mu)
-            K[..., 2 * N + 1, 2 * N] += (mu * q - 2.0 * mu)
-            K[..., 2 * N + 1, 2 * N + 1] += (mu * s * q)
+            K[:, 2 * N, 2 * N] += mu * r * q
+            K[:, 2 * N, 2 * N + 1] += mu * q - 2.0 * mu
+            K[:, 2 * N + 1, 2 * N] += mu * q - 2.0 * mu
+            K[:, 2 * N + 1, 2 * N + 1] += mu * s * q
             continue
-        he = h[e].item()
-        Cr, Sr, Cs, Ss = torch.cosh(k * r * he), torch.sinh(k * r * he), torch.cosh(k * s * he), torch.sinh(k * s * he)
+        kh = kc * float(h[e])
+        Cr, Sr = torch.cosh(kh * r), torch.sinh(kh * r)
+        Cs, Ss = torch.cosh(kh * s), torch.sinh(kh * s)
         D = 2.0 * (1.0 - Cr * Cs) + (1.0 / (r * s) + r * s) * Sr * Ss
-        f = k * rh * cp * cp / D
+        f = kc * rh * c2 / D
         k11 = f * (Cr * Ss / s - r * Sr * Cs)
-        k12 = f * (Cr * Cs - r * s * Sr * Ss - 1.0) - k * rh * be * be * (1.0 + s * s)
+        k12 = f * (Cr * Cs - r * s * Sr * Ss - 1.0) - kc * (rh * be * be) * (1.0 + s * s)
         k13 = f * (r * Sr - Ss / s)
         k14 = f * (Cs - Cr)
         k22 = f * (Sr * Cs / r - s * Cr * Ss)
         k24 = f * (s * Ss - Sr / r)
-        Ke = [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12], [k14, k24, -k12, k22]]
+        Ke = [[k11, k12, k13, k14], [k12, k22, -k14, k24], [k13, -k14, k11, -k12],
+              [k14, k24, -k12, k22]]
         for a in range(4):
             for b in range(4):
-                K[..., 2 * e + a, 2 * e + b] += Ke[a][b]
+                K[:, 2 * e + a, 2 * e + b] += Ke[a][b]
     return K
 
 
-def first_change(sign):
-    """Algorithm 1 on a full sign grid [rows, V]: idx of the first change, -1 if none."""
-    ch = sign[:, 1:] != sign[:, :-1]
-    anyc = ch.any(1)
-    idx = torch.argmax(ch.to(torch.int8), dim=1) + 1
-    return torch.where(anyc, idx, torch.full_like(idx, -1))
+def dense_det_points(h, alpha, beta, rho, lam_pts, c_pts):
+    """det K by dense assembly + batched LU at explicit points (used by tests/test_gpu_f2.py)."""
+    cp = perturb(c_pts, alpha, beta)
+    return torch.linalg.det(dense_K(h, alpha, beta, rho, TWO_PI / lam_pts, cp))
 
 
-def timed(fn, reps=5):
-    fn()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
+class Timer:
+    def __init__(self):
+        self.ms = 0.0
+
+    def __call__(self, fn):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         out = fn()
         e1.record()
         e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    return statistics.median(ts), out
+        self.ms += e0.elapsed_time(e1)
+        return out
 
 
-def one_model(name, w, reps=5):
+def full_grid(name, w, lam_override=None):
+    dev = torch.device("cuda:0")
     m = w.models
     h, al, be, rh = (torch.as_tensor(x[0], device=dev) for x in (m.h, m.alpha, m.beta, m.rho))
-    lam, c = torch.as_tensor(w.lam, device=dev), torch.as_tensor(w.c, device=dev)
+    lam_np = w.lam if lam_override is None else lam_override
+    lam, c = torch.as_tensor(lam_np, device=dev), torch.as_tensor(w.c, device=dev)
     L, V = lam.shape[0], c.shape[0]
+    P = L * V
+    n = 2 * (m.n_layers + 1)
 
-    def dense():
-        K = dense_K(h, al, be, rh, lam, c)
-        return torch.linalg.det(K)
+    # banded: every det value on the grid (warm-up, then timed)
+    masw.masw_det_grid(h, al, be, rh, lam, c)
+    tb = Timer()
+    re, im, ex2 = tb(lambda: masw.masw_det_grid(h, al, be, rh, lam, c))
+    band_sign = torch.sign(re).reshape(-1)
+    del im, ex2
+    # product path: early-exit curve (algorithmic dets)
+    masw.masw_curve(h, al, be, rh, lam, c)
+    tc = Timer()
+    tc(lambda: masw.masw_curve(h, al, be, rh, lam, c))
+    alg, _ = masw.masw_last_work()
 
-    def dense_assemble_only():
-        return dense_K(h, al, be, rh, lam, c)
-
-    t_dense, det = timed(dense, reps)
-    t_asm, _ = timed(dense_assemble_only, reps)
-    idx_dense = first_change(torch.sign(det.real)).cpu().numpy()
-    t_band, grid = timed(lambda: masw.masw_det_grid(h, al, be, rh, lam, c), reps)
-    t_curve, cur = timed(lambda: masw.masw_curve(h, al, be, rh, lam, c), reps)
-    idx_band = cur.idx.cpu().numpy()
-    gsign = torch.sign(grid[0]).cpu().numpy()
-    return {"grid": f"{L} x {V}", "dets": L * V,
-            "dense_assemble_plus_lu_ms": t_dense, "dense_assemble_ms": t_asm,
-            "dense_lu_ms": t_dense - t_asm,
-            "banded_full_grid_ms": t_band, "banded_early_exit_curve_ms": t_curve,
-            "speedup_full_grid_banded_vs_dense": t_dense / t_band,
-            "speedup_lu_only": (t_dense - t_asm) / t_band,
-            "ct_idx_equal": bool(np.array_equal(idx_dense, idx_band)),
-            "grid_sign_agreement": float(np.mean(gsign == torch.sign(det.real).cpu().numpy())),
-            "dense_bytes_per_matrix": (2 * (m.n_layers + 1)) ** 2 * 16}
+    cp_all = perturb(c, al, be)
+    k_all = TWO_PI / lam
+    t_asm, t_lu = Timer(), Timer()
+    agree = 0
+    disagree = 0
+    # warm-up of the dense arm on one small chunk
+    torch.linalg.det(dense_K(h, al, be, rh, k_all[:1].repeat(1024), cp_all[:1024]))
+    for p0 in range(0, P, CHUNK):
+        p = torch.arange(p0, min(P, p0 + CHUNK), device=dev)
+        i, j = p // V, p % V
+        K = t_asm(lambda: dense_K(h, al, be, rh, k_all[i], cp_all[j]))
+        det = t_lu(lambda: torch.linalg.det(K))
+        del K
+        ds = torch.sign(det.real)
+        same = int((ds == band_sign[p0:p0 + p.shape[0]]).sum())
+        agree += same
+        disagree += int(p.shape[0]) - same
+    dense_total = t_asm.ms + t_lu.ms
+    return {
+        "grid": f"{L} x {V} (one N={m.n_layers} model, {name})", "dets": P,
+        "dense_bytes_per_matrix": n * n * 16,
+        "dense_chunk_matrices": CHUNK,
+        "dense_assemble_ms": t_asm.ms, "dense_lu_ms": t_lu.ms, "dense_total_ms": dense_total,
+        "dense_lu_dets_per_s": P / (t_lu.ms * 1e-3),
+        "dense_total_dets_per_s": P / (dense_total * 1e-3),
+        "banded_det_grid_ms": tb.ms, "banded_det_grid_dets_per_s": P / (tb.ms * 1e-3),
+        "speedup_banded_vs_dense_lu_only": t_lu.ms / tb.ms,
+        "speedup_banded_vs_dense_assemble_plus_lu": dense_total / tb.ms,
+        "early_exit_curve_ms": tc.ms, "early_exit_algorithmic_dets": alg,
+        "early_exit_algorithmic_dets_per_s": alg / (tc.ms * 1e-3),
+        "sign_re_det_agree": agree, "sign_re_det_disagree": disagree,
+    }
 
 
 def main():
     out = {"paper": "PAPER.md:147: banded GE kernel ~10x faster than cublasZgetrfBatched on a "
                     "Quadro K620 (sm_50); cuBLAS LU was >50% of GPU time",
-           "C1_tiny": one_model("tiny", synth.workload("tiny")),
-           "C2_variable40": one_model("maswaves", synth.workload("maswaves")),
-           "C3_uniform_N10_sample": one_model("uniform", synth.workload("uniform", L=8), reps=3)}
+           "device": torch.cuda.get_device_name(0),
+           "dense_lu": "torch.linalg.det (batched complex128 getrf from the vendor libraries)",
+           "C4_realistic_N5_full_grid": full_grid("realistic", synth.workload("realistic")),
+           # C3's model and grid; the three tier wavelengths (PAPER.md:238 analog) in turn
+           "C3_uniform_N10_1000x10000": full_grid(
+               "uniform, lambda = 1/30/200 m in turn", synth.workload("uniform"),
+               lam_override=np.tile([1.0, 30.0, 200.0], 334)[:1000])}
     path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/dense_lu_baseline.json"
     json.dump(out, open(path, "w"), indent=1)
     print(json.dumps(out, indent=1))

@@ -727,14 +727,20 @@ def test_async_scan_timing_ring(masw):
 
 
 @pytest.mark.parametrize("team", [1, 4])
-def test_static_schedules_same_results_and_team_counts(masw, team):
-    """The paper's static partitions as scan schedules: identical C_t, and the
-    per-team det counts add up to the algorithmic total."""
+def test_static_schedules_same_results_and_team_counts(masw, orc, team):
+    """The paper's static partitions as scan schedules: the oracle's C_t under
+    every schedule (queue, contiguous, modular), and the per-team det counts add up to the
+    oracle's algorithmic total Sum(idx + 1)."""
     w = synth.workload("ensemble", M=500)
     m = w.models
     args = (m.h, m.alpha, m.beta, m.rho, w.lam, w.c, w.ce)
+    o = orc.ensemble(m, w.lam, w.c, w.ce)
     ref = masw.masw_curves_ensemble(*args, team_warps=team, flags=masw.TEAM_STATS)
+    assert np.array_equal(ref.idx, o["idx"])
+    for k in range(len(ref.misfit)):
+        assert parity.misfit_ok(orc, ref.ct[k], w.ce, float(ref.misfit[k]))
     alg_ref, _ = masw.masw_last_work()
+    assert alg_ref == int(np.where(o["idx"] >= 0, o["idx"] + 1, len(w.c)).sum())
     tq = masw.masw_last_team_dets()
     assert tq is not None and int(tq.sum()) == alg_ref
     for fl in (masw.SCHED_CONTIGUOUS, masw.SCHED_MODULAR):

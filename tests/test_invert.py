@@ -89,3 +89,20 @@ def test_invert_cli_on_gpu(tmp_path):
     assert len(rows) == 6
     best = float(rows[1].split(",")[2])
     assert best < 0.05                       # the C2 model lies inside these bounds
+    # every reported model's misfit is the oracle's for that model (CSV values are exact
+    # reprs; Algorithm 2 on the oracle's Algorithm 1 curve)
+    import oracle
+
+    N = 5
+    prev = -1.0
+    for row in rows[1:]:
+        f = row.split(",")
+        mis = float(f[2])
+        x = [float(v) for v in f[3:]]
+        h, a, b, r = x[:N], x[N:2 * N + 1], x[2 * N + 1:3 * N + 2], x[3 * N + 2:]
+        st, ct, idx, nd = oracle.curve(h, a, b, r, w.lam, w.c)
+        assert st == 0
+        mst, om = oracle.misfit(ct, w.ce)
+        assert abs(mis - om) <= 1e-9 * abs(om), (mis, om)
+        assert mis >= prev                   # ranked by misfit
+        prev = mis
