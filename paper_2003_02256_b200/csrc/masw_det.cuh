@@ -108,16 +108,44 @@ static __constant__ double c_k[4] = {
 // coincide (broadcast reads).
 constexpr unsigned kExpTabBytes = kExpTabN * 16u;
 
+// The fine variant of the table (g_cosh_sinh_fine: d = 1/128, th < 44.37) and its element
+// functions are used for calls whose largest k h is at most kFineKhMax: every wave argument
+// th = k h x is below k h (x = sqrt(1 - c^2/v^2) < 1), so the fine table covers it.  The
+// scans choose per call from the validation pass (ws_fine), all of them by the same test, so
+// they stay bitwise identical to one another.  (The scaled elements of MASW_STABLE reach
+// th = 354 and always use the coarse table.)
+#ifndef MASW_FINE_KH_MAX
+#define MASW_FINE_KH_MAX 44.0
+#endif
+constexpr double kFineKhMax = MASW_FINE_KH_MAX;
+struct FineTab {
+    unsigned a;   // 32-bit shared address of the fine rows
+};
+template <class TabT> struct TabTraits {
+    static constexpr double inv_d = kExpInvD;
+    static __device__ __forceinline__ const double2 *rows() { return g_cosh_sinh; }
+    static __device__ __forceinline__ unsigned make(unsigned a) { return a; }
+};
+template <> struct TabTraits<FineTab> {
+    static constexpr double inv_d = kExpFInvD;
+    static __device__ __forceinline__ const double2 *rows() { return g_cosh_sinh_fine; }
+    static __device__ __forceinline__ FineTab make(unsigned a) { return FineTab{a}; }
+};
+
+// rows of the table a launch can reach (m <= kh_max / d + 1)
+template <class TabT = unsigned>
 __device__ __forceinline__ int exp_rows_needed(double kh_max)
 {
-    const double m = kh_max * kExpInvD + 2.0;
+    const double m = kh_max * TabTraits<TabT>::inv_d + 2.0;
     return (m < (double)kExpTabN) ? (int)m : kExpTabN;   // (NaN -> all rows)
 }
 
+template <class TabT = unsigned>
 __device__ __forceinline__ void exp_scale_fill(void *tab, int rows)
 {
     double2 *t2 = reinterpret_cast<double2 *>(tab);
-    for (int m = threadIdx.x; m < rows; m += blockDim.x) t2[m] = g_cosh_sinh[m];
+    const double2 *src = TabTraits<TabT>::rows();
+    for (int m = threadIdx.x; m < rows; m += blockDim.x) t2[m] = src[m];
 }
 
 // Shared-memory addressing with 32-bit shared-window addresses held in registers.  The
@@ -180,6 +208,10 @@ __device__ __forceinline__ LayerConst load_lc_at(unsigned a)
     return L;
 }
 
+// The cosh/sinh table (below) as the element functions read it: a 32-bit shared-memory
+// address (every scan copies the table into shared memory).
+__device__ __forceinline__ double2 tab_load(unsigned tab, unsigned m) { return lds_v2(tab + m * 16u); }
+
 // The MUFU fp64 seeds (rcp.approx.ftz.f64, rsqrt.approx.ftz.f64) have relative error
 // e <= 2^-20.1 on sm_100a (scripts/mufu_accuracy.cu, measured on B200), so ONE higher-order
 // correction reaches full precision: its truncation error is O(e^3) ~ 2^-60.
@@ -222,7 +254,8 @@ __device__ __forceinline__ void sqrt_rsqrt(double q, double &x, double &rx)
 // At m = 0 (A = 1, B = 0) sinh th = O exactly structured (no cancellation at small th); for
 // m >= 1, B and A O do not cancel (th >= m d / 2).  15 FP64 operations, no branch (the
 // table covers th < 354.97; the index is clamped so a NaN argument stays in bounds).
-__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, unsigned tab)
+template <class TabT>
+__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, TabT tab)
 {
     // th + 1.5 * 2^52 d rounds th to the nearest multiple of d (ulp d); its low word is m.
     // Three DADDs with immediate operands (no constant materialisation); r is exact
@@ -240,10 +273,36 @@ __device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, uns
 #pragma unroll
     for (int i = 2; i < 4; ++i) po = fma(po, u, c_expO3[i]);
     const double E = pe * u, O = po * r;
+    const double2 ab = tab_load(tab, m);
+    const double A = ab.x, B = ab.y;
+    ch = fma(A, E, fma(B, O, A));
+    sh = fma(B, E, fma(A, O, B));
+}
+
+// The fine variant (FineTab: calls with k h <= kFineKhMax, see there): d = 1/128, |r| <= 1/256,
+// E = u (c0 u + c1) and O = r (c0' u^2 + c1' u + 1) (masw_exp_table.h: the same accuracy as
+// the coarse polynomials above): 13 FP64 operations instead of 15.
+__device__ __forceinline__ void cosh_sinh_fine(double th, double &ch, double &sh, unsigned tab)
+{
+    constexpr double kShifterF = kShifter * kExpFD;       // 1.5 * 2^45 (low word zero)
+    const double t = th + kShifterF;
+    const double md = t - kShifterF;                       // m d
+    const unsigned m = min((unsigned)__double2loint(t), (unsigned)(kExpTabN - 1));
+    const double r = th - md;                              // exact
+    const double u = r * r;
+    const double pe = fma(kExpFE1_0, u, c_expFE1[1]);      // E / r^2
+    double po = fma(kExpFO2_0, u, c_expFO2[1]);            // O / r
+    po = fma(po, u, c_expFO2[2]);
+    const double E = pe * u, O = po * r;
     const double2 ab = lds_v2(tab + m * 16u);
     const double A = ab.x, B = ab.y;
     ch = fma(A, E, fma(B, O, A));
     sh = fma(B, E, fma(A, O, B));
+}
+
+__device__ __forceinline__ void cosh_sinh(double th, double &ch, double &sh, FineTab tab)
+{
+    cosh_sinh_fine(th, ch, sh, tab.a);
 }
 
 // sin and cos of th in [0, 8e5] (< 2^19 pi/2: 3-part Cody-Waite reduction, the first product
@@ -323,8 +382,9 @@ __device__ __forceinline__ void sin_cos_reduced(double r, int n, double &sn, dou
 
 // -------------------------------------------------------------- wave triples
 // (C, XS, SX) of one wave: q = 1 - c^2/v^2 (!= 0 by S4) and kh = k*h; see header comment.
+template <class TabT>
 __device__ __forceinline__ void wave_hyp(double q, double kh, double &C, double &XS, double &SX,
-                                         unsigned tab)
+                                         TabT tab)
 {
     double x, rq;                      // x, 1/x
     sqrt_rsqrt(q, x, rq);
@@ -351,8 +411,9 @@ __device__ __forceinline__ void wave_trig(double q, double kh, double &C, double
     SX = sn * rq;
 }
 
+template <class TabT>
 __device__ __forceinline__ void wave_triple(double q, double kh, double &C, double &XS,
-                                            double &SX, unsigned tab)
+                                            double &SX, TabT tab)
 {
     if (q > 0.0) {
         wave_hyp(q, kh, C, XS, SX, tab);
@@ -441,15 +502,17 @@ __device__ __forceinline__ double lc_kappa(const LayerConst &L, double ic2)
 
 // Rare case c > alpha_e (both waves possibly trigonometric): kept out of line so the hot
 // loop's code stays small (instruction-cache pressure was measured: no_instruction stalls).
+template <class TabT>
 static __device__ __noinline__ void waves_general(double qa, double qb, double kh, double *t,
-                                                  unsigned tab)
+                                                  TabT tab)
 {
     wave_triple(qa, kh, t[0], t[1], t[2], tab);
     wave_triple(qb, kh, t[3], t[4], t[5], tab);
 }
 
+template <class TabT>
 __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
-                                           unsigned tab)
+                                           TabT tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
     const double qb = fma(-c2, L.ib2, 1.0);   // s^2
@@ -474,8 +537,9 @@ __device__ __forceinline__ Elem layer_elem(const LayerConst &L, double c2,
 }
 
 // layer_elem without the factor f (ElemU; ic2 = 1/c^2 of the same c2).
+template <class TabT>
 __device__ __forceinline__ ElemU layer_elem_u(const LayerConst &L, double c2, double ic2,
-                                              unsigned tab)
+                                              TabT tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0);   // r^2
     const double qb = fma(-c2, L.ib2, 1.0);   // s^2
@@ -521,7 +585,8 @@ struct ExpScaled {
     double c, s, e;   // cosh(x) e^-x, sinh(x) e^-x, e^-x   (x in [0, 700])
 };
 
-__device__ __forceinline__ ExpScaled exp_scaled(double x, unsigned tab)
+template <class TabT>
+__device__ __forceinline__ ExpScaled exp_scaled(double x, TabT tab)
 {
     ExpScaled o;
     if (x <= kExpSplit) {
@@ -542,8 +607,9 @@ __device__ __forceinline__ ExpScaled exp_scaled(double x, unsigned tab)
 
 // Both waves hyperbolic (c < beta_e < alpha_e); entries as described above, all scaled by
 // e^-(th_r + th_s) in numerator and denominator (f = f^ e^-(th_r + th_s)).
+template <class TabT>
 __device__ __forceinline__ Elem elem_stable_hh(double kh, double c2, double ia2, double ib2,
-                                               double krho, double mu, unsigned tab)
+                                               double krho, double mu, TabT tab)
 {
     const double a = c2 * ia2, b = c2 * ib2;
     double r, rr, s, rsn;
@@ -573,8 +639,9 @@ __device__ __forceinline__ Elem elem_stable_hh(double kh, double c2, double ia2,
 
 // P wave hyperbolic, S wave trigonometric (beta_e < c < alpha_e): the direct formulas with
 // the P-wave terms scaled by e^-th_r (overflow-free for th_r up to 700).
+template <class TabT>
 __device__ __forceinline__ Elem elem_stable_ht(double kh, double c2, double ia2, double ib2,
-                                               double krho, double mu, unsigned tab)
+                                               double krho, double mu, TabT tab)
 {
     double r, rr;
     sqrt_rsqrt(fma(-c2, ia2, 1.0), r, rr);
@@ -595,7 +662,8 @@ __device__ __forceinline__ Elem elem_stable_ht(double kh, double c2, double ia2,
     return E;
 }
 
-__device__ __forceinline__ Elem layer_elem_stable(const LayerConst &L, double c2, unsigned tab)
+template <class TabT>
+__device__ __forceinline__ Elem layer_elem_stable(const LayerConst &L, double c2, TabT tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0), qb = fma(-c2, L.ib2, 1.0);
     if (qa > 0.0 && qb > 0.0) return elem_stable_hh(L.kh, c2, L.ia2, L.ib2, L.krho, lc_mu(L), tab);
@@ -609,8 +677,9 @@ __device__ __forceinline__ Elem layer_elem_stable(const LayerConst &L, double c2
 // scaled brackets and the scaled D^ are one consistent pair (f^ D^ = k rho c^2), so U = the
 // brackets with k12's correction as kappa D^ -- the f-free recursion runs on them unchanged,
 // and every entry stays O(1) for k h up to 700 (no overflow in D_t d_t either).
+template <class TabT>
 __device__ __forceinline__ ElemU elemu_stable_hh(double kh, double c2, double ia2, double ib2,
-                                                 double kap, double rratio, unsigned tab)
+                                                 double kap, double rratio, TabT tab)
 {
     const double a = c2 * ia2, b = c2 * ib2;
     double r, rr, s, rsn;
@@ -638,8 +707,9 @@ __device__ __forceinline__ ElemU elemu_stable_hh(double kh, double c2, double ia
     return U;
 }
 
+template <class TabT>
 __device__ __forceinline__ ElemU elemu_stable_ht(double kh, double c2, double ia2, double ib2,
-                                                 double kap, double rratio, unsigned tab)
+                                                 double kap, double rratio, TabT tab)
 {
     double r, rr;
     sqrt_rsqrt(fma(-c2, ia2, 1.0), r, rr);
@@ -662,8 +732,9 @@ __device__ __forceinline__ ElemU elemu_stable_ht(double kh, double c2, double ia
 
 // layer_elem_stable without the factor; L.kh = k h (row scan) -- the model-major and pair
 // scans pass a copy with k h formed from their k-free h (the same product).
+template <class TabT>
 __device__ __forceinline__ ElemU layer_elemu_stable(const LayerConst &L, double c2, double ic2,
-                                                    unsigned tab)
+                                                    TabT tab)
 {
     const double qa = fma(-c2, L.ia2, 1.0), qb = fma(-c2, L.ib2, 1.0);
     const double kap = lc_kappa(L, ic2);
@@ -689,9 +760,10 @@ __device__ __forceinline__ double2 wave_root(double q)
     return make_double2(q > 0.0 ? x : -x, rx);
 }
 
+template <class TabT>
 __device__ __forceinline__ void wave_hyp_root(double x, double rx, double kh, double &C,
                                               double &XS, double &SX,
-                                              unsigned tab)
+                                              TabT tab)
 {
     double ch, sh;
     cosh_sinh(kh * x, ch, sh, tab);
@@ -720,9 +792,10 @@ __device__ __forceinline__ void wave_trig_root(double xneg, double rx, double kh
 // M holds the model's k-free constants: M.kh = h, M.krho = rho, M.b2 = 2 beta^2; only
 // k h = k * M.kh depends on the wavelength (formed exactly as the row scan's LayerConst
 // fill forms it, so both scans compute bitwise-identical elements).
+template <class TabT>
 __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, double2 a,
                                                 double2 b, double c2,
-                                                unsigned tab)
+                                                TabT tab)
 {
     const double kh = k * M.kh;
     double Cr, XSr, SXr, Cs, XSs, SXs;
@@ -746,8 +819,9 @@ __device__ __forceinline__ Elem layer_elem_root(const LayerConst &M, double k, d
 // Elements of layer M for two wavenumbers ka, kb (two wavelengths of one model) at the same
 // velocity: one branch on the wave types, both rows' waves interleaved inside it.  Each
 // row's arithmetic is exactly layer_elem_root's (bitwise-identical elements).
+template <class TabT>
 __device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka, double kb,
-                                                 double2 a, double2 b, double c2, unsigned tab,
+                                                 double2 a, double2 b, double c2, TabT tab,
                                                  Elem &Ea, Elem &Eb)
 {
     const double kha = ka * M.kh, khb = kb * M.kh;
@@ -780,9 +854,10 @@ __device__ __forceinline__ void layer_elem_root2(const LayerConst &M, double ka,
 }
 
 // layer_elem_root / layer_elem_root2 without the factor f (ElemU), for the sign scans.
+template <class TabT>
 __device__ __forceinline__ ElemU layer_elem_root_u(const LayerConst &M, double k, double2 a,
                                                    double2 b, double c2, double ic2,
-                                                   unsigned tab)
+                                                   TabT tab)
 {
     const double kh = k * M.kh;
     double Cr, XSr, SXr, Cs, XSs, SXs;
@@ -803,9 +878,10 @@ __device__ __forceinline__ ElemU layer_elem_root_u(const LayerConst &M, double k
     return elemu_from_triples(Cr, XSr, SXr, Cs, XSs, SXs, lc_kappa(M, ic2), M.aux);
 }
 
+template <class TabT>
 __device__ __forceinline__ void layer_elem_root2_u(const LayerConst &M, double ka, double kb,
                                                    double2 a, double2 b, double c2, double ic2,
-                                                   unsigned tab, ElemU &Ea, ElemU &Eb)
+                                                   TabT tab, ElemU &Ea, ElemU &Eb)
 {
     const double kha = ka * M.kh, khb = kb * M.kh;
     double Cra, XSra, SXra, Csa, XSsa, SXsa;
@@ -1548,10 +1624,10 @@ __device__ __forceinline__ void det_sign_block_pair(int N, Elem2Fn &&elem2, Hs2F
 // `vel` (shared memory).  `maybe_near` = false means c is already the S4-perturbed velocity
 // (the scan resolves S4 per warp for its 32 velocities, see scan_kernel), which skips the
 // per-lane S4 loop.
-template <bool WANT_VALUE, int NFIX = 0, bool STABLE = false>
+template <bool WANT_VALUE, int NFIX = 0, bool STABLE = false, class TabT = unsigned>
 __device__ __forceinline__ DetOut det_K(const LayerConst *__restrict__ lc,
                                         const double *__restrict__ vel,
-                                        unsigned tab, int Nrt, double c,
+                                        TabT tab, int Nrt, double c,
                                         bool maybe_near = true)
 {
     const int N = NFIX > 0 ? NFIX : Nrt;

@@ -54,12 +54,23 @@ __device__ __forceinline__ bool ws_range_bad(const Workspace *ws, bool stable)
     return kmax * h_max > (stable ? kMaxKHStable : kMaxKH);
 }
 
-// max over the call's rows and layers of k h_e (validated: <= 350) -> cosh/sinh table rows.
-__device__ __forceinline__ int ws_exp_rows(const Workspace *ws)
+// max over the call's rows and layers of k h_e (validated: <= 350)
+__device__ __forceinline__ double ws_kh_max(const Workspace *ws)
 {
     const double lam_min = __longlong_as_double((long long)~ws->lam_min_nbits);
     const double h_max = __longlong_as_double((long long)ws->h_max_bits);
-    return exp_rows_needed((kTwoPi / lam_min) * h_max);
+    return (kTwoPi / lam_min) * h_max;
+}
+// -> rows of the cosh/sinh table the call can reach
+template <class TabT = unsigned>
+__device__ __forceinline__ int ws_exp_rows(const Workspace *ws)
+{
+    return exp_rows_needed<TabT>(ws_kh_max(ws));
+}
+// the call's direct elements take the fine cosh/sinh table (FineTab, masw_det.cuh)
+__device__ __forceinline__ bool ws_fine(const Workspace *ws)
+{
+    return ws_kh_max(ws) <= kFineKhMax;
 }
 
 // grid_mask selects which grid_err bits make the call invalid.
@@ -599,16 +610,16 @@ constexpr int scan_min_blocks()
 #ifndef MASW_BLOCK_SIGN
 #define MASW_BLOCK_SIGN 1
 #endif
-template <bool STABLE>
+template <bool STABLE, class TabT>
 static __device__ __noinline__ int row_det_gepp(const LayerConst *lc, const double *vel,
-                                                unsigned ta, int N, double c)
+                                                TabT ta, int N, double c)
 {
     const DetOut d = det_K<false, 0, STABLE>(lc, vel, ta, N, c, false);
     return d.bad ? 2 : d.sign;
 }
 
-template <int TEAM, int BLOCK, bool STABLE>
-__global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(ScanArgs a)
+template <int TEAM, int BLOCK, bool STABLE, class TabT>
+__device__ __forceinline__ void scan_kernel_body(ScanArgs a)
 {
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     extern __shared__ __align__(16) unsigned char smem[];
@@ -634,9 +645,9 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     }
     __syncthreads();
     if (s_abort) return;
-    exp_scale_fill(tab, ws_exp_rows(ws));
+    exp_scale_fill<TabT>(tab, ws_exp_rows<TabT>(ws));
     __syncthreads();
-    const unsigned ta = opaque(smem_addr(tab));
+    const TabT ta = TabTraits<TabT>::make(opaque(smem_addr(tab)));
     // rows with a small-c prefix (reading S15''; smallc_prefix_kernel ran before this kernel)
     const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;
 
@@ -853,6 +864,24 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
     }
 }
 
+// The direct element's cosh/sinh table (FineTab where the call allows it, ws_fine) is a
+// kernel template parameter: the launcher enqueues both instances and the one that does not
+// match the call returns at once (the table choice needs the validation pass, which runs on
+// the device; one kernel holding both bodies behind a run-time branch was measured slower:
+// C5 38.89 ms vs 37.85 ms for the fine body alone).
+template <class TabT>
+__device__ __forceinline__ bool tab_mismatch(const Workspace *ws)
+{
+    return ws_fine(ws) != std::is_same<TabT, FineTab>::value;
+}
+
+template <int TEAM, int BLOCK, bool STABLE, class TabT>
+__global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(ScanArgs a)
+{
+    if (!STABLE && tab_mismatch<TabT>(a.ws)) return;
+    scan_kernel_body<TEAM, BLOCK, STABLE, TabT>(a);
+}
+
 // ------------------------------------------------------------------ model-major scan
 // For ensembles (many models): a warp takes a WORK ITEM = one model and up to kModelRows of
 // its wavelengths, and scans the velocity chunks in ascending order for all of the item's
@@ -914,9 +943,9 @@ __device__ __forceinline__ LayerConst with_kh(LayerConst M, double kh)
     return M;
 }
 
-template <bool STABLE>
+template <bool STABLE, class TabT>
 static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, unsigned ha,
-                                                   unsigned ta, double k,
+                                                   TabT ta, double k,
                                                    double c2, int N)
 {
     const DetOut d = det_core<false, 0, 1>(
@@ -934,8 +963,8 @@ static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, uns
     return d.bad ? 2 : d.sign;
 }
 
-template <bool STABLE>
-__global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a)
+template <bool STABLE, class TabT>
+__device__ __forceinline__ void scan_models_body(ScanArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_abort;
@@ -960,9 +989,9 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     }
     __syncthreads();
     if (s_abort) return;
-    exp_scale_fill(tab, ws_exp_rows(ws));
+    exp_scale_fill<TabT>(tab, ws_exp_rows<TabT>(ws));
     __syncthreads();
-    const unsigned ta = opaque(smem_addr(tab));
+    const TabT ta = TabTraits<TabT>::make(opaque(smem_addr(tab)));
     const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;   // reading S15''
 
     const int64_t M = a.mod.M, L = a.L;
@@ -1294,6 +1323,13 @@ __global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a
     }
 }
 
+template <bool STABLE, class TabT>
+__global__ void __launch_bounds__(kModelsBlock, 1) scan_models_kernel(ScanArgs a)
+{
+    if (!STABLE && tab_mismatch<TabT>(a.ws)) return;
+    scan_models_body<STABLE, TabT>(a);
+}
+
 // ------------------------------------------------------------------ pair scan (one long curve)
 // Single curves with many wavelengths (C3, C4): a warp pops TWO consecutive rows of the one
 // model and scans them in lockstep -- each lane evaluates both rows at its velocity with the
@@ -1317,8 +1353,8 @@ __host__ __device__ inline unsigned pair_smem_bytes(int N)
 }
 
 // GEPP sign for one lane of the pair scan (roots formed on the fly, as the row scan forms them)
-template <bool STABLE>
-static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, unsigned ta,
+template <bool STABLE, class TabT>
+static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, TabT ta,
                                                  double k, double c2, int N)
 {
     const DetOut d = det_core<false, 0, 1>(
@@ -1336,8 +1372,8 @@ static __device__ __noinline__ int pair_det_gepp(unsigned ma, unsigned ha, unsig
     return d.bad ? 2 : d.sign;
 }
 
-template <bool STABLE>
-__global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
+template <bool STABLE, class TabT>
+__device__ __forceinline__ void scan_pair_body(ScanArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_abort;
@@ -1357,9 +1393,9 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
     }
     __syncthreads();
     if (s_abort) return;
-    exp_scale_fill(tab, ws_exp_rows(ws));
+    exp_scale_fill<TabT>(tab, ws_exp_rows<TabT>(ws));
     __syncthreads();
-    const unsigned ta = opaque(smem_addr(tab));
+    const TabT ta = TabTraits<TabT>::make(opaque(smem_addr(tab)));
 
     const bool prefix = a.pstart != nullptr && ws->prefix_rows != 0ull;   // reading S15''
     const int64_t M = a.mod.M, L = a.L;
@@ -1622,6 +1658,13 @@ __global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
     }
 }
 
+template <bool STABLE, class TabT>
+__global__ void __launch_bounds__(kPairBlock, 1) scan_pair_kernel(ScanArgs a)
+{
+    if (!STABLE && tab_mismatch<TabT>(a.ws)) return;
+    scan_pair_body<STABLE, TabT>(a);
+}
+
 // Per-device launch facts, cached: SM count and resident CTAs per SM per (kernel, smem).
 namespace {
 std::mutex g_cache_mu;
@@ -1725,7 +1768,8 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
     constexpr int TEAMS = BLOCK / (32 * TEAM);
     const size_t smem = kExpTabBytes + round16((unsigned)sizeof(TeamCtrl) * TEAMS) +
                         (size_t)TEAMS * team_model_bytes(a.mod.N);
-    auto kern = scan_kernel<TEAM, BLOCK, STABLE>;
+    auto kern = scan_kernel<TEAM, BLOCK, STABLE, unsigned>;
+    auto kfine = scan_kernel<TEAM, BLOCK, false, FineTab>;   // (see tab_mismatch)
     const int sms = sm_count(device);
     const long long key = ((long long)device << 48) | ((long long)STABLE << 40) |
                           ((long long)TEAM << 32) | (long long)smem;
@@ -1737,6 +1781,7 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
     }
     {
         cudaError_t e = ensure_smem_optin(kern, device, 16 + TEAM + (STABLE ? 32 : 0));
+        if (e == cudaSuccess && !STABLE) e = ensure_smem_optin(kfine, device, 64 + TEAM);
         if (e != cudaSuccess) return e;
     }
     if (per_sm == 0) {
@@ -1755,6 +1800,10 @@ static cudaError_t launch_scan_t(const ScanArgs &a, cudaStream_t st, int device,
     if (dry) return cudaSuccess;
     kern<<<(unsigned)blocks, BLOCK, smem, st>>>(a);
     count_launch();
+    if (!STABLE) {
+        kfine<<<(unsigned)blocks, BLOCK, smem, st>>>(a);
+        count_launch();
+    }
     return cudaGetLastError();
 }
 
@@ -1817,7 +1866,8 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
 {
     const int wpc = models_warps(a.mod.N, device);
     const size_t smem = kExpTabBytes + (size_t)wpc * (size_t)warp_model_bytes(a.mod.N);
-    auto kern = a.stable ? scan_models_kernel<true> : scan_models_kernel<false>;
+    auto kern = a.stable ? scan_models_kernel<true, unsigned> : scan_models_kernel<false, unsigned>;
+    auto kfine = scan_models_kernel<false, FineTab>;   // (see tab_mismatch)
     const int sms = sm_count(device);
     const long long key = ((long long)device << 48) | (1ll << 47) | (a.stable ? (1ll << 46) : 0ll) |
                           ((long long)wpc << 32) |
@@ -1834,7 +1884,8 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
         if (wpc == 0) {
             per_sm = -1;
         } else {
-            if (ensure_smem_optin(kern, device, a.stable ? 5 : 1) != cudaSuccess) {
+            if (ensure_smem_optin(kern, device, a.stable ? 5 : 1) != cudaSuccess ||
+                (!a.stable && ensure_smem_optin(kfine, device, 8) != cudaSuccess)) {
                 cudaGetLastError();
                 per_sm = -1;
             } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpc,
@@ -1869,6 +1920,10 @@ static cudaError_t launch_models(const ScanArgs &a, cudaStream_t st, int device,
     }
     kern<<<(unsigned)blocks, 32 * wpc, smem, st>>>(b);
     count_launch();
+    if (!a.stable) {
+        kfine<<<(unsigned)blocks, 32 * wpc, smem, st>>>(b);
+        count_launch();
+    }
     return cudaGetLastError();
 }
 
@@ -2020,7 +2075,8 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
                                 size_t *scratch_bytes = nullptr)
 {
     const size_t smem = pair_smem_bytes(a.mod.N);
-    auto kern = a.stable ? scan_pair_kernel<true> : scan_pair_kernel<false>;
+    auto kern = a.stable ? scan_pair_kernel<true, unsigned> : scan_pair_kernel<false, unsigned>;
+    auto kfine = scan_pair_kernel<false, FineTab>;   // (see tab_mismatch)
     const int sms = sm_count(device);
     const long long key = ((long long)device << 48) | (2ll << 44) | (a.stable ? (1ll << 43) : 0ll) |
                           (long long)smem;
@@ -2032,6 +2088,7 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
     }
     if (per_sm == 0) {
         if (ensure_smem_optin(kern, device, a.stable ? 6 : 4) != cudaSuccess ||
+            (!a.stable && ensure_smem_optin(kfine, device, 9) != cudaSuccess) ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPairBlock, smem) !=
                 cudaSuccess) {
             cudaGetLastError();
@@ -2075,6 +2132,10 @@ static cudaError_t launch_pairs(const ScanArgs &a, cudaStream_t st, int device,
     }
     kern<<<(unsigned)blocks, kPairBlock, smem, st>>>(b);
     count_launch();
+    if (!a.stable) {
+        kfine<<<(unsigned)blocks, kPairBlock, smem, st>>>(b);
+        count_launch();
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !b.tail_pairs) return e;
     pair_tail_combine_kernel<<<(unsigned)((2 * b.tail_pairs * 32 + kCombineBlock - 1) / kCombineBlock),

@@ -92,13 +92,45 @@ def across_workers(name, w, reps):
     return res
 
 
+def across_workers_ensemble(w, reps):
+    """The same partitions at throughput scale: every worker scans ALL models of the C5
+    ensemble on its share of the 40 wavelengths (masw_curves_ensemble on device-resident
+    inputs), so a worker's device time follows its det count instead of launch latency."""
+    m = w.models
+    args = [t(x) for x in (m.h, m.alpha, m.beta, m.rho)]
+    c = t(w.c)
+    st, ct, idx, _ = masw.masw_curves_ensemble(*args, t(w.lam), c)
+    ix = idx.cpu().numpy()
+    work = np.where(ix >= 0, ix + 1, len(w.c)).astype(np.int64).sum(axis=0)   # per wavelength
+    W = len(w.lam)
+    res = {}
+    t1 = d1 = None
+    for strat in ("contiguous", "modular"):
+        res[strat] = {}
+        for G in range(1, 9):
+            parts = D.partition_wavelengths(W, G, strat)
+            dets = [int(work[p].sum()) for p in parts]
+            times = []
+            for p in parts:
+                lam_p = t(w.lam[p])
+                times.append(time_ms(lambda: masw.masw_curves_ensemble(*args, lam_p, c),
+                                     reps=reps))
+            if t1 is None:
+                t1, d1 = times[0], dets[0]
+            res[strat][G] = {"worker_dets": dets, "worker_ms": [round(x, 4) for x in times],
+                             "det_speedup": d1 / max(dets), "time_speedup": t1 / max(times)}
+    return res
+
+
 def main():
     out = {"within_gpu": {
         "C4_realistic_team1": within_gpu("realistic", synth.workload("realistic"), 1),
         "C5_ensemble_team1": within_gpu("ensemble", synth.workload("ensemble", M=100_000), 1)},
         "across_workers": {
         "C2_variable40": across_workers("maswaves", synth.workload("maswaves"), 20),
-        "C4_realistic": across_workers("realistic", synth.workload("realistic"), 3)}}
+        "C4_realistic": across_workers("realistic", synth.workload("realistic"), 3),
+        "C5_ensemble_variable40": across_workers_ensemble(
+            synth.workload("ensemble", M=100_000), 3)}}
     path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/load_balance.json"
     json.dump(out, open(path, "w"), indent=1)
     for k, v in out["within_gpu"].items():
