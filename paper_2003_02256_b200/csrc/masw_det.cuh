@@ -106,16 +106,17 @@ static __constant__ double c_k[4] = {
 // copies only the rows the launch can reach (m <= kh_max / d + 1, kh_max = max k h over the
 // call's rows and layers).  Lanes of a warp hold neighbouring velocities, so their m mostly
 // coincide (broadcast reads).
-constexpr unsigned kExpTabBytes = kExpTabN * 16u;
+// shared-memory bytes reserved for the table (the larger of the coarse and fine ones)
+constexpr unsigned kExpTabBytes = (kExpTabN > kExpTabNF ? kExpTabN : kExpTabNF) * 16u;
 
-// The fine variant of the table (g_cosh_sinh_fine: d = 1/128, th < 44.37) and its element
+// The fine variant of the table (g_cosh_sinh_fine: d = 1/128, th < 49.49) and its element
 // functions are used for calls whose largest k h is at most kFineKhMax: every wave argument
 // th = k h x is below k h (x = sqrt(1 - c^2/v^2) < 1), so the fine table covers it.  The
 // scans choose per call from the validation pass (ws_fine), all of them by the same test, so
 // they stay bitwise identical to one another.  (The scaled elements of MASW_STABLE reach
 // th = 354 and always use the coarse table.)
 #ifndef MASW_FINE_KH_MAX
-#define MASW_FINE_KH_MAX 44.0
+#define MASW_FINE_KH_MAX 49.0
 #endif
 constexpr double kFineKhMax = MASW_FINE_KH_MAX;
 struct FineTab {
@@ -123,11 +124,13 @@ struct FineTab {
 };
 template <class TabT> struct TabTraits {
     static constexpr double inv_d = kExpInvD;
+    static constexpr int n = kExpTabN;
     static __device__ __forceinline__ const double2 *rows() { return g_cosh_sinh; }
     static __device__ __forceinline__ unsigned make(unsigned a) { return a; }
 };
 template <> struct TabTraits<FineTab> {
     static constexpr double inv_d = kExpFInvD;
+    static constexpr int n = kExpTabNF;
     static __device__ __forceinline__ const double2 *rows() { return g_cosh_sinh_fine; }
     static __device__ __forceinline__ FineTab make(unsigned a) { return FineTab{a}; }
 };
@@ -136,8 +139,9 @@ template <> struct TabTraits<FineTab> {
 template <class TabT = unsigned>
 __device__ __forceinline__ int exp_rows_needed(double kh_max)
 {
+    constexpr int n = TabTraits<TabT>::n;
     const double m = kh_max * TabTraits<TabT>::inv_d + 2.0;
-    return (m < (double)kExpTabN) ? (int)m : kExpTabN;   // (NaN -> all rows)
+    return (m < (double)n) ? (int)m : n;   // (NaN -> all rows)
 }
 
 template <class TabT = unsigned>
@@ -287,7 +291,7 @@ __device__ __forceinline__ void cosh_sinh_fine(double th, double &ch, double &sh
     constexpr double kShifterF = kShifter * kExpFD;       // 1.5 * 2^45 (low word zero)
     const double t = th + kShifterF;
     const double md = t - kShifterF;                       // m d
-    const unsigned m = min((unsigned)__double2loint(t), (unsigned)(kExpTabN - 1));
+    const unsigned m = min((unsigned)__double2loint(t), (unsigned)(kExpTabNF - 1));
     const double r = th - md;                              // exact
     const double u = r * r;
     const double pe = fma(kExpFE1_0, u, c_expFE1[1]);      // E / r^2

@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(BLOCK, scan_min_blocks<BLOCK>()) scan_kernel(S
 #ifndef MASW_MODELS_UNROLL
 #define MASW_MODELS_UNROLL 1
 #endif
-constexpr int kModelRows = 48;   // wavelengths per work item (C5: 40, one item per model)
+constexpr int kModelRows = 40;   // wavelengths per work item (C5: 40, one item per model)
 #ifndef MASW_TAIL_ROWS
 #define MASW_TAIL_ROWS 8
 #endif
@@ -920,18 +920,25 @@ constexpr int kModelsMinWarps = 12;
 
 // Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
 // velocities (S4), k per row, the first grid index per row (small-c prefix, reading S15''),
-// the carried sign per row, then per lane (lane-major, stride 32N + 48 bytes = an odd
-// number of 16-byte units, so the lanes' 128-bit loads are conflict-free): the roots
-// (x_a, 1/|x_a|), (x_b, 1/|x_b|) of every layer, the half-space (r, s), (gw, t) and case.
-__host__ __device__ inline unsigned lane_cache_stride(int N) { return 32u * (unsigned)N + 48u; }
-__host__ __device__ inline unsigned warp_model_bytes(int N)
+// the carried sign per row, then the lanes' caches of 2N + 2 16-byte slots each, slot-major
+// (slot q of lane l at 512 q + 16 l: a warp's 128-bit loads of one slot are contiguous and
+// conflict-free): the roots (x_a, 1/|x_a|), (x_b, 1/|x_b|) of every layer (slots 2e, 2e + 1)
+// and the half-space's k-free factors (r, s), (gw, t') (HsRoot; t' = t, +0 or -0 encodes the
+// case, see hs_from_cache).  (32 N + 32 bytes per lane: with 16 warps at N = 6 this leaves
+// room for the fine cosh/sinh table.)
+__host__ __device__ inline unsigned lane_cache_stride(int N) { return 32u * (unsigned)N + 32u; }
+constexpr unsigned kSlot = 512u;   // bytes between consecutive slots of one lane
+__host__ __device__ inline unsigned models_cache_off(int N)
 {
     return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
                    2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
                    (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
                    (unsigned)kModelRows * (unsigned)sizeof(int32_t) +      // first index per row
-                   (unsigned)kModelRows +                                  // carried sign per row (s8)
-                   32u * lane_cache_stride(N));                            // per-lane roots
+                   (unsigned)kModelRows);                                  // carried sign per row (s8)
+}
+__host__ __device__ inline unsigned warp_model_bytes(int N)
+{
+    return models_cache_off(N) + 32u * lane_cache_stride(N);              // + the lanes' caches
 }
 
 // GEPP sign for one lane of the model-major kernel (see row_det_gepp); the same element
@@ -951,10 +958,10 @@ static __device__ __noinline__ int models_det_gepp(unsigned ma, unsigned ca, uns
     const DetOut d = det_core<false, 0, 1>(
         N,
         [&](int e) {
-            const unsigned o = 32u * (unsigned)e;
+            const unsigned o = 2u * kSlot * (unsigned)e;
             const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
             if constexpr (STABLE) return layer_elem_stable(with_kh(M, k * M.kh), c2, ta);
-            else return layer_elem_root(M, k, lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
+            else return layer_elem_root(M, k, lds_v2(ca + o), lds_v2(ca + o + kSlot), c2, ta);
         },
         [&] {
             const LayerConst H = load_lc_at(ha);   // as the row scan's GEPP forms it
@@ -978,8 +985,7 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
     double *kr = vel + 2 * (N + 1);
     int32_t *jst = reinterpret_cast<int32_t *>(kr + kModelRows);             // per row: first index
     signed char *carry = reinterpret_cast<signed char *>(jst + kModelRows);  // per row: last sign
-    const unsigned stride = lane_cache_stride(N);
-    unsigned char *cl = reinterpret_cast<unsigned char *>(carry + kModelRows) + (unsigned)lane * stride;
+    unsigned char *cl = wb + models_cache_off(N) + 16u * (unsigned)lane;   // slot 0 of this lane
 
     Workspace *ws = a.ws;
     if (threadIdx.x == 0) {
@@ -1104,21 +1110,20 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
             const double ic2 = rcp_fast(c2);
             // wavelength-free terms of this lane's velocity (lane-private slots: no sync)
             {
-                double2 *rt = reinterpret_cast<double2 *>(cl);
+                double2 *rt = reinterpret_cast<double2 *>(cl);   // slot q at rt[32 q]
                 for (int e = 0; e < N; ++e) {
                     const LayerConst Lc = mc[e];
-                    rt[2 * e] = wave_root(fma(-c2, Lc.ia2, 1.0));
-                    rt[2 * e + 1] = wave_root(fma(-c2, Lc.ib2, 1.0));
+                    rt[64 * e] = wave_root(fma(-c2, Lc.ia2, 1.0));
+                    rt[64 * e + 32] = wave_root(fma(-c2, Lc.ib2, 1.0));
                 }
-                // the half-space element as BlockSignU takes it: K_hs / (rho_(N-1) c^2)
+                // the half-space's k-free factors; hs_from_cache forms the element per pair
                 const LayerConst Hl = mc[N];
-                const HalfSpace H = halfspace_k(halfspace_root(Hl.ia2, Hl.ib2, c2), Hl.aux * ic2);
-                rt[2 * N] = make_double2(H.h11r, H.h12r);
-                rt[2 * N + 1] = make_double2(H.h22r, H.h11i);
-                rt[2 * N + 2] = make_double2(H.h12i, H.h22i);
+                const HsRoot R = halfspace_root(Hl.ia2, Hl.ib2, c2);
+                rt[64 * N] = make_double2(R.r, R.s);
+                rt[64 * N + 32] = make_double2(R.gw, R.kase == 1 ? R.t : (R.kase == 0 ? 0.0 : -0.0));
             }
             const unsigned ca = opaque(smem_addr(cl));
-            const unsigned hca = ca + 32u * (unsigned)N;
+            const unsigned hca = ca + 2u * kSlot * (unsigned)N;
             // chunks below some row's small-c prefix end (reading S15''): only the rows whose
             // scan starts before the chunk's end take part; lanes below a row's start take the
             // prefix's sign
@@ -1164,17 +1169,18 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
                         sts_s8(ya + (unsigned)r, s);   // carried to the next chunk
                     }
                 };
-                auto hs_scaled = [&] {   // K_hs / (rho_(N-1) c^2), k-free (cached above)
-                    const double2 p = lds_v2(hca), q = lds_v2(hca + 16u), r = lds_v2(hca + 32u);
-                    HalfSpace H;
-                    H.h11r = p.x;
-                    H.h12r = p.y;
-                    H.h22r = q.x;
-                    H.h11i = q.y;
-                    H.h12i = r.x;
-                    H.h22i = r.y;
-                    H.real = __double2hiint(H.h11i) == 0;   // +0 exactly below beta_N
-                    return H;
+                // K_hs / (rho_(N-1) c^2), k-free: from the cached HsRoot (the case from t':
+                // t > 0 in case 1, +0 in case 0, -0 in case 2), formed as the row scan forms it
+                auto hs_scaled = [&] {
+                    const double2 p = lds_v2(hca), q = lds_v2(hca + kSlot);
+                    HsRoot R;
+                    R.r = p.x;
+                    R.s = p.y;
+                    R.gw = q.x;
+                    R.t = q.y;
+                    const int th = __double2hiint(q.y);
+                    R.kase = th > 0 ? 1 : (th < 0 ? 2 : 0);
+                    return halfspace_k(R, lds_f64(ha + 40u) * ic2);   // mu' = aux_N / c^2
                 };
 #if !MASW_BLOCK_SIGN
                 auto hs_gepp = [&] {     // K_hs / k, as the row scan's GEPP forms it
@@ -1198,14 +1204,14 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
                             det_sign_block_u_pair<MASW_MODELS_UNROLL>(
                                 N,
                                 [&](int e, ElemU &E1, ElemU &E2) {
-                                    const unsigned o = 32u * (unsigned)e;
+                                    const unsigned o = 2u * kSlot * (unsigned)e;
                                     const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
                                     if constexpr (STABLE) {
                                         E1 = layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
                                         E2 = layer_elemu_stable(with_kh(M, k2 * M.kh), c2, ic2, ta);
                                     } else {
                                         layer_elem_root2_u(M, k, k2, lds_v2(ca + o),
-                                                           lds_v2(ca + o + 16u), c2, ic2, ta, E1,
+                                                           lds_v2(ca + o + kSlot), c2, ic2, ta, E1,
                                                            E2);
                                     }
                                 },
@@ -1247,13 +1253,13 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
                             so = det_sign_block_u<MASW_MODELS_UNROLL>(
                                 N,
                                 [&](int e) {
-                                    const unsigned o = 32u * (unsigned)e;
+                                    const unsigned o = 2u * kSlot * (unsigned)e;
                                     const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
                                     if constexpr (STABLE)
                                         return layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
                                     else
                                         return layer_elem_root_u(M, k, lds_v2(ca + o),
-                                                                 lds_v2(ca + o + 16u), c2, ic2, ta);
+                                                                 lds_v2(ca + o + kSlot), c2, ic2, ta);
                                 },
                                 hs_scaled);
                         if (so.ok) {
@@ -1268,9 +1274,9 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
                         const DetOut d = det_core<false, 0, MASW_MODELS_UNROLL>(
                             N,
                             [&](int e) {
-                                const unsigned o = 32u * (unsigned)e;
+                                const unsigned o = 2u * kSlot * (unsigned)e;
                                 return layer_elem_root(load_lc_at(ma + 48u * (unsigned)e), k,
-                                                       lds_v2(ca + o), lds_v2(ca + o + 16u), c2, ta);
+                                                       lds_v2(ca + o), lds_v2(ca + o + kSlot), c2, ta);
                             },
                             hs_gepp);
                         s = d.sign;
