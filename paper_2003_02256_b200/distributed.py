@@ -141,7 +141,7 @@ def worst_status(st: int, device, group=None) -> int:
     every rank if any rank failed."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     sts = [int(st)]
-    if world > 1:
+    if dist.is_initialized():   # (also at world size 1: the same collective code path)
         t = torch.tensor([int(st)], dtype=torch.int64, device=device)
         sts = _all_gather_padded(t, [1] * world, group).tolist()
     lo, hi = min(sts), max(sts)
@@ -157,7 +157,7 @@ def _all_gather_padded(x: torch.Tensor, counts: Sequence[int], group=None) -> to
     all_gather_into_tensor, trim).  The same collective on every backend (NCCL on the GPU
     box, gloo in the CPU tests)."""
     world = len(counts)
-    if world == 1:
+    if world == 1 and not dist.is_initialized():
         return x
     mx = max(counts)
     if x.shape[0] == mx:
