@@ -109,14 +109,14 @@ static __constant__ double c_k[4] = {
 // shared-memory bytes reserved for the table (the larger of the coarse and fine ones)
 constexpr unsigned kExpTabBytes = (kExpTabN > kExpTabNF ? kExpTabN : kExpTabNF) * 16u;
 
-// The fine variant of the table (g_cosh_sinh_fine: d = 1/128, th < 49.49) and its element
+// The fine variant of the table (g_cosh_sinh_fine: d = 1/128, th < 50.55) and its element
 // functions are used for calls whose largest k h is at most kFineKhMax: every wave argument
 // th = k h x is below k h (x = sqrt(1 - c^2/v^2) < 1), so the fine table covers it.  The
 // scans choose per call from the validation pass (ws_fine), all of them by the same test, so
 // they stay bitwise identical to one another.  (The scaled elements of MASW_STABLE reach
 // th = 354 and always use the coarse table.)
 #ifndef MASW_FINE_KH_MAX
-#define MASW_FINE_KH_MAX 49.0
+#define MASW_FINE_KH_MAX 50.5
 #endif
 constexpr double kFineKhMax = MASW_FINE_KH_MAX;
 struct FineTab {
@@ -434,6 +434,21 @@ __device__ __forceinline__ double perturb_velocity(const double *__restrict__ ve
     for (;;) {
         bool near = false;
         for (int e = 0; e < nvel; ++e) near |= (fabs(c - vel[e]) < kPerturbTol);
+        if (!near) return c;
+        c = c * kPerturbFactor;
+    }
+}
+
+// The same for velocities held as separate alpha[0..n) and beta[0..n) arrays (the result
+// depends only on the set of velocities, so it equals perturb_velocity's bit for bit).
+__device__ __forceinline__ double perturb_velocity_ab(const double *__restrict__ al,
+                                                      const double *__restrict__ be, int n,
+                                                      double c)
+{
+    for (;;) {
+        bool near = false;
+        for (int e = 0; e < n; ++e)
+            near |= (fabs(c - al[e]) < kPerturbTol) | (fabs(c - be[e]) < kPerturbTol);
         if (!near) return c;
         c = c * kPerturbFactor;
     }

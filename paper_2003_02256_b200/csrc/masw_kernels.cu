@@ -918,8 +918,8 @@ constexpr int64_t kTailItemsPerWarp = MASW_TAIL_ITEMS;
 constexpr int kModelsBlock = MASW_MODELS_BLOCK;
 constexpr int kModelsMinWarps = 12;
 
-// Per-warp shared memory of the model-major scan: the model's k-free constants, its layer
-// velocities (S4), k per row, the first grid index per row (small-c prefix, reading S15''),
+// Per-warp shared memory of the model-major scan: the model's k-free constants, k per row,
+// the first grid index per row (small-c prefix, reading S15''),
 // the carried sign per row, then the lanes' caches of 2N + 2 16-byte slots each, slot-major
 // (slot q of lane l at 512 q + 16 l: a warp's 128-bit loads of one slot are contiguous and
 // conflict-free): the roots (x_a, 1/|x_a|), (x_b, 1/|x_b|) of every layer (slots 2e, 2e + 1)
@@ -931,7 +931,6 @@ constexpr unsigned kSlot = 512u;   // bytes between consecutive slots of one lan
 __host__ __device__ inline unsigned models_cache_off(int N)
 {
     return round16((unsigned)(N + 1) * (unsigned)sizeof(LayerConst) +     // model constants
-                   2u * (unsigned)(N + 1) * (unsigned)sizeof(double) +     // velocities (S4)
                    (unsigned)kModelRows * (unsigned)sizeof(double) +       // k per row
                    (unsigned)kModelRows * (unsigned)sizeof(int32_t) +      // first index per row
                    (unsigned)kModelRows);                                  // carried sign per row (s8)
@@ -981,8 +980,7 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
     unsigned char *tab = smem;
     unsigned char *wb = smem + kExpTabBytes + (unsigned)warp * warp_model_bytes(N);
     LayerConst *mc = reinterpret_cast<LayerConst *>(wb);
-    double *vel = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
-    double *kr = vel + 2 * (N + 1);
+    double *kr = reinterpret_cast<double *>(wb + (unsigned)(N + 1) * sizeof(LayerConst));
     int32_t *jst = reinterpret_cast<int32_t *>(kr + kModelRows);             // per row: first index
     signed char *carry = reinterpret_cast<signed char *>(jst + kModelRows);  // per row: last sign
     unsigned char *cl = wb + models_cache_off(N) + 16u * (unsigned)lane;   // slot 0 of this lane
@@ -1045,9 +1043,10 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
             x.aux = (e < N) ? rh / a.mod.rho[m * (N + 1) + e + 1]
                             : (rh * (be * be)) / a.mod.rho[m * (N + 1) + N - 1];
             mc[e] = x;
-            vel[2 * e] = al;
-            vel[2 * e + 1] = be;
         }
+        // the model's layer velocities (reading S4) are read from global memory (L1) per chunk
+        const double *__restrict__ mal = a.mod.alpha + m * (N + 1);
+        const double *__restrict__ mbe = a.mod.beta + m * (N + 1);
         // rows of the item in two 32-bit halves: pending = not yet found.  Small-c prefix
         // (reading S15''): row r's scan starts at jst[r] with carried sign carry[r]; rows the
         // prefix kernel finished are not pending.  smax / smin: largest / smallest start.
@@ -1091,20 +1090,18 @@ __device__ __forceinline__ void scan_models_body(ScanArgs a)
             const int j = base + lane;
             const bool valid = j < V;
             double c = cg[valid ? j : V - 1];
-            {   // reading S4, as in scan_kernel
+            {   // reading S4, as in scan_kernel (velocity i = 2e + w: alpha_e, beta_e)
                 const double clo = __shfl_sync(FULL, c, 0) - 1e-3;
                 const double chi = __shfl_sync(FULL, c, 31) + 1e-3;
                 bool lane_near = false;
                 for (int e0 = 0; e0 < nv; e0 += 32) {
-                    bool in = false;
-                    if (e0 + lane < nv) {
-                        const double v = vel[e0 + lane];
-                        in = (v > clo) && (v < chi);
-                    }
+                    const int i = e0 + lane;
+                    const double v = (i < nv) ? ((i & 1) ? mbe : mal)[i >> 1] : 0.0;
+                    const bool in = (i < nv) && (v > clo) && (v < chi);
                     for (unsigned b = __ballot_sync(FULL, in); b; b &= b - 1)
-                        lane_near |= fabs(c - vel[e0 + __ffs(b) - 1]) < kPerturbTol;
+                        lane_near |= fabs(c - __shfl_sync(FULL, v, __ffs(b) - 1)) < kPerturbTol;
                 }
-                if (lane_near) c = perturb_velocity(vel, nv, c);
+                if (lane_near) c = perturb_velocity_ab(mal, mbe, N + 1, c);
             }
             const double c2 = c * c;
             const double ic2 = rcp_fast(c2);
@@ -1938,7 +1935,7 @@ bool models_scan_suitable(const ScanArgs &a, int device, bool forced)
     // unless forced: enough work items to fill the GPU several times over and several
     // wavelengths per model to share the cache; and one CTA per SM of >= kModelsMinWarps
     // warps with the table and the per-warp caches must fit (16 warps for N <= 6, 14 for
-    // N = 7, 13 for N = 8)
+    // N = 7, 12 for N = 8)
     const int64_t items = a.mod.M * ((a.L + kModelRows - 1) / kModelRows);
     const int sms = sm_count(device);
     if (a.sched != 0) return false;
