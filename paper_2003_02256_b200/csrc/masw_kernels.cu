@@ -1432,219 +1432,228 @@ __device__ __forceinline__ void scan_pair_body(ScanArgs a)
             pi = Ph + tp;
             seg_lo = seg * SEGV;
         }
-        const int seg_hi = (seg < 0) ? V : min(V, seg_lo + SEGV);
-        const int64_t ip = pi / M, m = pi - ip * M;
-        const int64_t i0 = 2 * ip;
-        const bool two = i0 + 1 < L;
-        if (m != cur_m) {   // this model's k-free constants (as the model-major scan fills them)
-            __syncwarp();
-            for (int e = lane; e <= N; e += 32) {
-                const double al = a.mod.alpha[m * (N + 1) + e], be = a.mod.beta[m * (N + 1) + e];
-                const double rh = a.mod.rho[m * (N + 1) + e];
-                LayerConst x;
-                x.kh = (e < N) ? a.mod.h[m * N + e] : 0.0;
-                x.ia2 = 1.0 / (al * al);
-                x.ib2 = 1.0 / (be * be);
-                x.krho = rh;
-                x.b2 = 2.0 * (be * be);
-                x.aux = (e < N) ? rh / a.mod.rho[m * (N + 1) + e + 1]
-                                : (rh * (be * be)) / a.mod.rho[m * (N + 1) + N - 1];
-                mc[e] = x;
-                vel[2 * e] = al;
-                vel[2 * e + 1] = be;
-            }
-            __syncwarp();
-            cur_m = m;
-        }
-        const unsigned ma = opaque(smem_addr(mc));
-        const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
-        const long long r0 = m * L + i0;                        // output row of wavelength i0
-        const double k0 = kTwoPi / a.lam[i0];                   // reading S2
-        const double k1 = two ? kTwoPi / a.lam[i0 + 1] : k0;
-        // small-c prefixes (reading S15''): row q starts at js_q with carried sign pc_q, or
-        // was finished by smallc_prefix_kernel (js_q = -1)
-        int js0 = 0, js1 = 0, pc0 = 0, pc1 = 0;
-        if (prefix) {
-            js0 = a.pstart[r0];
-            pc0 = a.pcarry[r0];
-            if (two) {
-                js1 = a.pstart[r0 + 1];
-                pc1 = a.pcarry[r0 + 1];
-            }
-        }
-        int carry0 = pc0, carry1 = pc1;
-        bool pend0 = js0 >= 0, pend1 = two && js1 >= 0;
-        if (seg >= 0) {   // rows with an event in an earlier segment need no more segments
-            if (pend0 && *(volatile int *)&a.seg_found[2 * tp] < seg_lo) pend0 = false;
-            if (pend1 && *(volatile int *)&a.seg_found[2 * tp + 1] < seg_lo) pend1 = false;
-        }
-        const bool rec0 = seg >= 0 && pend0, rec1 = seg >= 0 && pend1;   // write a record
-        int fs0 = 0, fs1 = 0;            // segment: sign at seg_lo
-        int ev0 = -1, ev1 = -1;          // segment: in-segment event index
-        bool eb0 = false, eb1 = false;   // segment: the event is a non-finite det
-        const int jlo = (seg >= 0) ? seg_lo
-                      : ((pend0 && pend1) ? min(js0, js1) : (pend0 ? js0 : (pend1 ? js1 : 0)));
-        const int jfirst = (seg >= 0) ? seg_lo : 0;   // no predecessor to compare with
-        for (int base = (jlo / 32) * 32; base < seg_hi && (pend0 || pend1); base += 32) {
-            const int j = base + lane;
-            const bool valid = j < seg_hi;
-            double c = cg[valid ? j : V - 1];
-            {   // reading S4, as in scan_kernel
-                const double clo = __shfl_sync(FULL, c, 0) - 1e-3;
-                const double chi = __shfl_sync(FULL, c, 31) + 1e-3;
-                bool lane_near = false;
-                for (int e0 = 0; e0 < nv; e0 += 32) {
-                    bool in = false;
-                    if (e0 + lane < nv) {
-                        const double v = vel[e0 + lane];
-                        in = (v > clo) && (v < chi);
-                    }
-                    for (unsigned b = __ballot_sync(FULL, in); b; b &= b - 1)
-                        lane_near |= fabs(c - vel[e0 + __ffs(b) - 1]) < kPerturbTol;
+        // the item's scan, instantiated for whole pairs and for tail segments (SEG): the
+        // whole-pair loop carries none of the segment bookkeeping
+        auto item_body = [&](auto segc) {
+            constexpr bool SEG = decltype(segc)::value;
+            const int seg_hi = (!SEG) ? V : min(V, seg_lo + SEGV);
+            const int64_t ip = pi / M, m = pi - ip * M;
+            const int64_t i0 = 2 * ip;
+            const bool two = i0 + 1 < L;
+            if (m != cur_m) {   // this model's k-free constants (as the model-major scan fills them)
+                __syncwarp();
+                for (int e = lane; e <= N; e += 32) {
+                    const double al = a.mod.alpha[m * (N + 1) + e], be = a.mod.beta[m * (N + 1) + e];
+                    const double rh = a.mod.rho[m * (N + 1) + e];
+                    LayerConst x;
+                    x.kh = (e < N) ? a.mod.h[m * N + e] : 0.0;
+                    x.ia2 = 1.0 / (al * al);
+                    x.ib2 = 1.0 / (be * be);
+                    x.krho = rh;
+                    x.b2 = 2.0 * (be * be);
+                    x.aux = (e < N) ? rh / a.mod.rho[m * (N + 1) + e + 1]
+                                    : (rh * (be * be)) / a.mod.rho[m * (N + 1) + N - 1];
+                    mc[e] = x;
+                    vel[2 * e] = al;
+                    vel[2 * e + 1] = be;
                 }
-                if (lane_near) c = perturb_velocity(vel, nv, c);
+                __syncwarp();
+                cur_m = m;
             }
-            const double c2 = c * c;
-            const double ic2 = rcp_fast(c2);
-            int s0 = 0, s1 = 0;
-            bool bad0 = false, bad1 = false;
-            if (valid) {
-                const LayerConst Hl = load_lc_at(ha);
-                const HalfSpace H = halfspace_k(halfspace_root(Hl.ia2, Hl.ib2, c2), Hl.aux * ic2);
-                if (pend0 && pend1) {
-                    SignOut o0, o1;
-                    det_sign_block_u_pair<MASW_MODELS_UNROLL>(
-                        N,
-                        [&](int e, ElemU &E0, ElemU &E1) {
-                            const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
-                            if constexpr (STABLE) {
-                                E0 = layer_elemu_stable(with_kh(M, k0 * M.kh), c2, ic2, ta);
-                                E1 = layer_elemu_stable(with_kh(M, k1 * M.kh), c2, ic2, ta);
-                            } else {
-                                layer_elem_root2_u(M, k0, k1, wave_root(fma(-c2, M.ia2, 1.0)),
-                                                   wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta,
-                                                   E0, E1);
-                            }
-                        },
-                        [&](HalfSpace &H0, HalfSpace &H1) {
-                            H0 = H;
-                            H1 = H;
-                        },
-                        o0, o1);
-                    if (o0.ok) {
-                        s0 = o0.sign;
-                    } else {
-                        const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k0, c2, N);
-                        bad0 = (rr == 2);
-                        s0 = bad0 ? 0 : rr;
-                        ++my_fb;
-                    }
-                    if (o1.ok) {
-                        s1 = o1.sign;
-                    } else {
-                        const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k1, c2, N);
-                        bad1 = (rr == 2);
-                        s1 = bad1 ? 0 : rr;
-                        ++my_fb;
-                    }
-                    my_eval += 2;
-                } else {
-                    const double k = pend0 ? k0 : k1;
-                    const SignOut o = det_sign_block_u<MASW_MODELS_UNROLL>(
-                        N,
-                        [&](int e) {
-                            const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
-                            if constexpr (STABLE)
-                                return layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
-                            else
-                                return layer_elem_root_u(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
-                                                         wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2,
-                                                         ta);
-                        },
-                        [&] { return H; });
-                    int s = 0;
-                    bool bad = false;
-                    if (o.ok) {
-                        s = o.sign;
-                    } else {
-                        const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k, c2, N);
-                        bad = (rr == 2);
-                        s = bad ? 0 : rr;
-                        ++my_fb;
-                    }
-                    if (pend0) { s0 = s; bad0 = bad; } else { s1 = s; bad1 = bad; }
-                    ++my_eval;
+            const unsigned ma = opaque(smem_addr(mc));
+            const unsigned ha = ma + (unsigned)N * (unsigned)sizeof(LayerConst);
+            const long long r0 = m * L + i0;                        // output row of wavelength i0
+            const double k0 = kTwoPi / a.lam[i0];                   // reading S2
+            const double k1 = two ? kTwoPi / a.lam[i0 + 1] : k0;
+            // small-c prefixes (reading S15''): row q starts at js_q with carried sign pc_q, or
+            // was finished by smallc_prefix_kernel (js_q = -1)
+            int js0 = 0, js1 = 0, pc0 = 0, pc1 = 0;
+            if (prefix) {
+                js0 = a.pstart[r0];
+                pc0 = a.pcarry[r0];
+                if (two) {
+                    js1 = a.pstart[r0 + 1];
+                    pc1 = a.pcarry[r0 + 1];
                 }
             }
-            if (j < js0) {   // evaluated by the small-c prefix
-                s0 = pc0;
-                bad0 = false;
+            int carry0 = pc0, carry1 = pc1;
+            bool pend0 = js0 >= 0, pend1 = two && js1 >= 0;
+            if (SEG) {   // rows with an event in an earlier segment need no more segments
+                if (pend0 && *(volatile int *)&a.seg_found[2 * tp] < seg_lo) pend0 = false;
+                if (pend1 && *(volatile int *)&a.seg_found[2 * tp + 1] < seg_lo) pend1 = false;
             }
-            if (j < js1) {
-                s1 = pc1;
-                bad1 = false;
-            }
-            // first-sign-change bookkeeping of one row for this chunk (as scan_kernel, TEAM 1);
-            // a tail segment records its first sign / event instead of writing the row
-            auto settle = [&](long long r, int s, bool bad, int &carry, bool &pend, int &fs,
-                              int &evj, bool &evb, int tq) {
-                int sprev = __shfl_up_sync(FULL, s, 1);
-                if (lane == 0) sprev = carry;
-                if (seg >= 0 && base == seg_lo) fs = __shfl_sync(FULL, s, 0);
-                const bool ev = valid && (bad || (j > jfirst && s != sprev));
-                const unsigned mask = __ballot_sync(FULL, ev);
-                if (mask) {
-                    const int first = base + (__ffs(mask) - 1);
-                    if (seg >= 0) {
-                        evj = first;
-                        evb = __shfl_sync(FULL, (int)bad, __ffs(mask) - 1) != 0;
-                        if (lane == 0) atomicMin(&a.seg_found[tq], first);
-                        team_alg += (unsigned long long)(first + 1 - seg_lo);
-                    } else if (j == first) {
-                        if (bad) {
-                            a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
-                            if (a.idx) a.idx[r] = -2;
-                            my_status |= 2u;
-                        } else {
-                            a.ct[r] = cg[j];
-                            if (a.idx) a.idx[r] = (int32_t)j;
+            const bool rec0 = SEG && pend0, rec1 = SEG && pend1;   // write a record
+            int fs0 = 0, fs1 = 0;            // segment: sign at seg_lo
+            int ev0 = -1, ev1 = -1;          // segment: in-segment event index
+            bool eb0 = false, eb1 = false;   // segment: the event is a non-finite det
+            const int jlo = (SEG) ? seg_lo
+                          : ((pend0 && pend1) ? min(js0, js1) : (pend0 ? js0 : (pend1 ? js1 : 0)));
+            const int jfirst = (SEG) ? seg_lo : 0;   // no predecessor to compare with
+            for (int base = (jlo / 32) * 32; base < seg_hi && (pend0 || pend1); base += 32) {
+                const int j = base + lane;
+                const bool valid = j < seg_hi;
+                double c = cg[valid ? j : V - 1];
+                {   // reading S4, as in scan_kernel
+                    const double clo = __shfl_sync(FULL, c, 0) - 1e-3;
+                    const double chi = __shfl_sync(FULL, c, 31) + 1e-3;
+                    bool lane_near = false;
+                    for (int e0 = 0; e0 < nv; e0 += 32) {
+                        bool in = false;
+                        if (e0 + lane < nv) {
+                            const double v = vel[e0 + lane];
+                            in = (v > clo) && (v < chi);
                         }
-                        my_alg += (unsigned long long)(j + 1);
+                        for (unsigned b = __ballot_sync(FULL, in); b; b &= b - 1)
+                            lane_near |= fabs(c - vel[e0 + __ffs(b) - 1]) < kPerturbTol;
                     }
-                    if (seg < 0) team_alg += (unsigned long long)(first + 1);
-                    pend = false;
+                    if (lane_near) c = perturb_velocity(vel, nv, c);
                 }
-                // the last valid lane's sign (the segment's last sign after its last chunk)
-                carry = __shfl_sync(FULL, s, min(31, seg_hi - 1 - base));
-            };
-            if (pend0) settle(r0, s0, bad0, carry0, pend0, fs0, ev0, eb0, (int)(2 * tp));
-            if (pend1) settle(r0 + 1, s1, bad1, carry1, pend1, fs1, ev1, eb1, (int)(2 * tp + 1));
-        }
-        if (seg >= 0) {   // the segment's records: event index, first / last sign, flags
-            if (lane == 0) {
-                if (rec0)
-                    a.seg_rec[(2 * tp) * S + seg] =
-                        make_int2(ev0, (fs0 + 1) | ((carry0 + 1) << 2) | ((int)eb0 << 4) | 32);
-                if (rec1)
-                    a.seg_rec[(2 * tp + 1) * S + seg] =
-                        make_int2(ev1, (fs1 + 1) | ((carry1 + 1) << 2) | ((int)eb1 << 4) | 32);
+                const double c2 = c * c;
+                const double ic2 = rcp_fast(c2);
+                int s0 = 0, s1 = 0;
+                bool bad0 = false, bad1 = false;
+                if (valid) {
+                    const LayerConst Hl = load_lc_at(ha);
+                    const HalfSpace H = halfspace_k(halfspace_root(Hl.ia2, Hl.ib2, c2), Hl.aux * ic2);
+                    if (pend0 && pend1) {
+                        SignOut o0, o1;
+                        det_sign_block_u_pair<MASW_MODELS_UNROLL>(
+                            N,
+                            [&](int e, ElemU &E0, ElemU &E1) {
+                                const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+                                if constexpr (STABLE) {
+                                    E0 = layer_elemu_stable(with_kh(M, k0 * M.kh), c2, ic2, ta);
+                                    E1 = layer_elemu_stable(with_kh(M, k1 * M.kh), c2, ic2, ta);
+                                } else {
+                                    layer_elem_root2_u(M, k0, k1, wave_root(fma(-c2, M.ia2, 1.0)),
+                                                       wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2, ta,
+                                                       E0, E1);
+                                }
+                            },
+                            [&](HalfSpace &H0, HalfSpace &H1) {
+                                H0 = H;
+                                H1 = H;
+                            },
+                            o0, o1);
+                        if (o0.ok) {
+                            s0 = o0.sign;
+                        } else {
+                            const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k0, c2, N);
+                            bad0 = (rr == 2);
+                            s0 = bad0 ? 0 : rr;
+                            ++my_fb;
+                        }
+                        if (o1.ok) {
+                            s1 = o1.sign;
+                        } else {
+                            const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k1, c2, N);
+                            bad1 = (rr == 2);
+                            s1 = bad1 ? 0 : rr;
+                            ++my_fb;
+                        }
+                        my_eval += 2;
+                    } else {
+                        const double k = pend0 ? k0 : k1;
+                        const SignOut o = det_sign_block_u<MASW_MODELS_UNROLL>(
+                            N,
+                            [&](int e) {
+                                const LayerConst M = load_lc_at(ma + 48u * (unsigned)e);
+                                if constexpr (STABLE)
+                                    return layer_elemu_stable(with_kh(M, k * M.kh), c2, ic2, ta);
+                                else
+                                    return layer_elem_root_u(M, k, wave_root(fma(-c2, M.ia2, 1.0)),
+                                                             wave_root(fma(-c2, M.ib2, 1.0)), c2, ic2,
+                                                             ta);
+                            },
+                            [&] { return H; });
+                        int s = 0;
+                        bool bad = false;
+                        if (o.ok) {
+                            s = o.sign;
+                        } else {
+                            const int rr = pair_det_gepp<STABLE>(ma, ha, ta, k, c2, N);
+                            bad = (rr == 2);
+                            s = bad ? 0 : rr;
+                            ++my_fb;
+                        }
+                        if (pend0) { s0 = s; bad0 = bad; } else { s1 = s; bad1 = bad; }
+                        ++my_eval;
+                    }
+                }
+                if (j < js0) {   // evaluated by the small-c prefix
+                    s0 = pc0;
+                    bad0 = false;
+                }
+                if (j < js1) {
+                    s1 = pc1;
+                    bad1 = false;
+                }
+                // first-sign-change bookkeeping of one row for this chunk (as scan_kernel, TEAM 1);
+                // a tail segment records its first sign / event instead of writing the row
+                auto settle = [&](long long r, int s, bool bad, int &carry, bool &pend, int &fs,
+                                  int &evj, bool &evb, int tq) {
+                    int sprev = __shfl_up_sync(FULL, s, 1);
+                    if (lane == 0) sprev = carry;
+                    if (SEG && base == seg_lo) fs = __shfl_sync(FULL, s, 0);
+                    const bool ev = valid && (bad || (j > jfirst && s != sprev));
+                    const unsigned mask = __ballot_sync(FULL, ev);
+                    if (mask) {
+                        const int first = base + (__ffs(mask) - 1);
+                        if (SEG) {
+                            evj = first;
+                            evb = __shfl_sync(FULL, (int)bad, __ffs(mask) - 1) != 0;
+                            if (lane == 0) atomicMin(&a.seg_found[tq], first);
+                            team_alg += (unsigned long long)(first + 1 - seg_lo);
+                        } else if (j == first) {
+                            if (bad) {
+                                a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                                if (a.idx) a.idx[r] = -2;
+                                my_status |= 2u;
+                            } else {
+                                a.ct[r] = cg[j];
+                                if (a.idx) a.idx[r] = (int32_t)j;
+                            }
+                            my_alg += (unsigned long long)(j + 1);
+                        }
+                        if (!SEG) team_alg += (unsigned long long)(first + 1);
+                        pend = false;
+                    }
+                    // the last valid lane's sign (the segment's last sign after its last chunk)
+                    carry = __shfl_sync(FULL, s, min(31, seg_hi - 1 - base));
+                };
+                if (pend0) settle(r0, s0, bad0, carry0, pend0, fs0, ev0, eb0, (int)(2 * tp));
+                if (pend1) settle(r0 + 1, s1, bad1, carry1, pend1, fs1, ev1, eb1, (int)(2 * tp + 1));
             }
-            team_alg += pend0 ? (unsigned long long)(seg_hi - seg_lo) : 0ull;   // no event
-            team_alg += pend1 ? (unsigned long long)(seg_hi - seg_lo) : 0ull;
-            continue;
-        }
-        for (int q = 0; q < 2; ++q) {
-            const bool p = q ? pend1 : pend0;
-            if (!p) continue;
-            team_alg += (unsigned long long)V;
-            if (lane == 0) {
-                const long long r = r0 + q;
-                a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
-                if (a.idx) a.idx[r] = -1;
-                my_status |= 1u;
-                my_alg += (unsigned long long)V;
+            if (SEG) {   // the segment's records: event index, first / last sign, flags
+                if (lane == 0) {
+                    if (rec0)
+                        a.seg_rec[(2 * tp) * S + seg] =
+                            make_int2(ev0, (fs0 + 1) | ((carry0 + 1) << 2) | ((int)eb0 << 4) | 32);
+                    if (rec1)
+                        a.seg_rec[(2 * tp + 1) * S + seg] =
+                            make_int2(ev1, (fs1 + 1) | ((carry1 + 1) << 2) | ((int)eb1 << 4) | 32);
+                }
+                team_alg += pend0 ? (unsigned long long)(seg_hi - seg_lo) : 0ull;   // no event
+                team_alg += pend1 ? (unsigned long long)(seg_hi - seg_lo) : 0ull;
+                return;
             }
-        }
+            for (int q = 0; q < 2; ++q) {
+                const bool p = q ? pend1 : pend0;
+                if (!p) return;
+                team_alg += (unsigned long long)V;
+                if (lane == 0) {
+                    const long long r = r0 + q;
+                    a.ct[r] = __longlong_as_double(0x7ff8000000000000ll);
+                    if (a.idx) a.idx[r] = -1;
+                    my_status |= 1u;
+                    my_alg += (unsigned long long)V;
+                }
+            }
+        };
+        if (seg >= 0)
+            item_body(std::true_type{});
+        else
+            item_body(std::false_type{});
     }
     if (a.team_dets && lane == 0)
         a.team_dets[(long long)blockIdx.x * (blockDim.x / 32) + warp] = team_alg;

@@ -769,3 +769,37 @@ def test_sharded_drivers_with_cuda_ops(masw, orc):
                              dev(e.lam), dev(e.c), dev(e.ce))
     o = orc.ensemble(em, e.lam, e.c, e.ce)
     assert np.array_equal(res.idx.cpu().numpy(), o["idx"]) and res.best == o["best"]
+
+
+def test_fine_and_coarse_table_calls_agree(masw, orc):
+    """The cosh/sinh table is chosen per call (fine d = 1/128 for k h_max <= 50.5, else the
+    coarse d = 1/16): the same rows scanned in a fine call and in a call that one
+    extra short wavelength pushes onto the coarse table give the oracle's index on both
+    sides (the two tables differ only by rounding, so an index could move only at a
+    near-root, rule S16)."""
+    e = synth.workload("ensemble", M=1500)
+    m = e.models
+    hmax = float(m.h.max())
+    assert 2 * math.pi / e.lam.min() * hmax <= 50.5          # the fine table
+    lam_x = 2 * math.pi * hmax / 52.0                        # k h_max = 52: the coarse table
+    lam2 = np.concatenate([e.lam, [lam_x]])
+    args = [dev(x) for x in (m.h, m.alpha, m.beta, m.rho)]
+    a = masw.masw_curves_ensemble(*args, dev(e.lam), dev(e.c))
+    b = masw.masw_curves_ensemble(*args, dev(lam2), dev(e.c))
+    ia = a.idx.cpu().numpy()
+    ib = b.idx.cpu().numpy()[:, : len(e.lam)]
+    o = orc.ensemble(m, e.lam, e.c)
+    assert np.array_equal(ia, o["idx"])
+    assert np.array_equal(ib, o["idx"])
+    # single curve through the pair scan: C4's model (k h_max 50.27, fine) and + lambda_x
+    w = synth.workload("realistic")
+    wm = w.models
+    sel = np.arange(0, len(w.lam), 25)                       # 400 of the 10k wavelengths
+    lam = w.lam[sel]
+    lamc = np.concatenate([lam, [2 * math.pi * float(wm.h[0].max()) / 52.0]])
+    mod = [dev(x[0]) for x in (wm.h, wm.alpha, wm.beta, wm.rho)]
+    st1, _, i1 = masw.masw_curve(*mod, dev(lam), dev(w.c), flags=masw.SCHED_PAIRS)
+    st2, _, i2 = masw.masw_curve(*mod, dev(lamc), dev(w.c), flags=masw.SCHED_PAIRS)
+    ost, _, oidx, _ = orc.curve(*margs(wm), lam, w.c)
+    assert np.array_equal(i1.cpu().numpy(), oidx)
+    assert np.array_equal(i2.cpu().numpy()[: len(lam)], oidx)
