@@ -1,6 +1,7 @@
 """Host-buffer path timing (development aid): one C5-size masw_curves_ensemble call with
-pinned host buffers, CUDA-event timed, for each MASW_HOST_CHUNKS setting given on the command
-line (each in its own process).
+pinned host buffers, CUDA-event timed, once per command-line argument, each in its own process
+with MASW_HOST_CHUNKS set to it (a knob of the measured, rejected pipelined-path build --
+DESIGN.md §10b; the current library ignores it, so every argument times the one-launch path).
 
     python scripts/host_path_time.py 1 2 4 8
 """
