@@ -19,7 +19,10 @@ PUBLIC_HEADERS = [os.path.join(ROOT, "include", "masw.h"), os.path.join(ROOT, "i
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr",
+         # ptxas register-usage heuristic at its most register-hungry setting (same-box A/B,
+         # profiles/r2/ptxas_reglevel_ab.txt: C4 -2.1 %, C3 -0.3 %, C5 unchanged; idx identical)
+         "-Xptxas", "-regUsageLevel=10"]
 
 
 def _inputs():
@@ -47,8 +50,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     objs = []
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s),
-               "-o", obj]
+        extra = os.environ.get("MASW_NVCC_EXTRA", "").split() if out is not None else []
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-c",
+               os.path.join(CSRC, s), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
