@@ -803,3 +803,32 @@ def test_fine_and_coarse_table_calls_agree(masw, orc):
     ost, _, oidx, _ = orc.curve(*margs(wm), lam, w.c)
     assert np.array_equal(i1.cpu().numpy(), oidx)
     assert np.array_equal(i2.cpu().numpy()[: len(lam)], oidx)
+
+
+@pytest.mark.parametrize("N,seed", [(1, 201), (3, 203), (5, 205), (8, 208)])
+def test_random_models_parity_fine_table(masw, orc, N, seed):
+    """The random-model property test on calls that take the FINE cosh/sinh table: the
+    shortest wavelength is chosen so that k h_max = 50.4 (<= 50.5), so wave arguments reach the
+    end of the table (th up to ~50); model-major and row scans bitwise equal, C_t against the
+    oracle under S16 with zero violations, from the 0.5 m/s grid start."""
+    mods = synth.random_models(120, N, seed)
+    hmax = float(mods.h.max())
+    lam = synth.geom(60.0, 2 * math.pi * hmax / 50.4, 24)
+    assert 2 * math.pi / lam.min() * hmax <= 50.5
+    c = 0.5 * (np.arange(1000, dtype=np.float64) + 1.0)
+    o = orc.ensemble(mods, lam, c, None)
+    st_m, ct_m, idx_m, _ = _ens(masw, mods, lam, c, None, masw.SCHED_MODELS, device=True)
+    st_r, ct_r, idx_r, _ = _ens(masw, mods, lam, c, None, masw.SCHED_ROWS, device=True)
+    assert st_m == st_r == o["status"]
+    assert np.array_equal(idx_m, idx_r) and np.array_equal(ct_m, ct_r, equal_nan=True)
+    bad = 0
+    for m in range(mods.n_models):
+        if np.array_equal(idx_m[m], o["idx"][m]):
+            continue
+        ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), lam, c, idx_m[m], o["idx"][m])
+        bad += int((~ok).sum())
+    assert bad == 0
+    for m in range(0, mods.n_models, 40):
+        a = [dev(x[m]) for x in (mods.h, mods.alpha, mods.beta, mods.rho)]
+        st_p, ct_p, idx_p = masw.masw_curve(*a, dev(lam), dev(c), flags=masw.SCHED_PAIRS)
+        assert np.array_equal(idx_p.cpu().numpy(), idx_r[m])
