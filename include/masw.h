@@ -146,7 +146,9 @@ typedef struct {
     void *cuda_stream;     /* cudaStream_t; NULL = legacy default stream                     */
     int32_t team_warps;    /* warps cooperating on one (model, lambda) row: 0 = auto, else a
                               power of two in [1, 16]; each step scans 32*team_warps
-                              consecutive velocities speculatively       */
+                              consecutive velocities speculatively.
+                              (SURVEY.md 8(b)'s chunk_width, counted in warps: chunk width
+                              = 32 * team_warps velocities.)                                */
     uint32_t flags;        /* MASW_* flags above                                             */
 } masw_exec;
 
@@ -161,7 +163,9 @@ int masw_curve(const masw_model *model, const double *lambda, int64_t L, const d
 
 /* Misfit of one curve (Algorithm 2): m = (1/L) sum_i |ct_i - ce_i| / ce_i.
  * +inf if any ct_i is NaN/Inf (reading S8).  Errors: L < 1 or null -> MASW_E_ARG;
- * ce NaN/Inf -> MASW_E_NONFINITE; ce <= 0 -> MASW_E_ARG.  misfit_out: one double. */
+ * ce NaN/Inf -> MASW_E_NONFINITE; ce <= 0 -> MASW_E_ARG.  misfit_out: one double.
+ * exec (nullable; an addition to SURVEY.md 8(b)'s signature): device and stream for
+ * device-pointer calls, as for the other entry points. */
 int masw_misfit(const double *ct, const double *ce, int64_t L, double *misfit_out,
                 const masw_exec *exec);
 
