@@ -1361,10 +1361,17 @@ __device__ __forceinline__ int exp_of(double x) { return (__double2hiint(x) >> 2
 // exponent fields): key(max|W'|) - key(d) <= kBlockMultExp << 20, i.e. the exponent
 // difference is at most kBlockMultExp and at most kBlockMultExp - 1 unless the top mantissa
 // bits of W' do not exceed d's (|W| < 2^13, typically <= 2^12: never looser than BlockSign's
-// exponent test); and every p nonzero normal and finite:
-// key(p) - key(DBL_MIN) < key(Inf) - key(DBL_MIN) as unsigned.
+// exponent test); and every p normal with a normal reciprocal, DBL_MIN <= |p| < 2^1022:
+// key(p) - key(DBL_MIN) < key(2^1022) - key(DBL_MIN) as unsigned.  (The reciprocal of p is
+// taken with rcp.approx.ftz, which flushes a subnormal result to zero: for 2^1022 <= |p| <
+// 2^1024 the recursion would silently drop the coupling to the layer above -- measured on
+// thick layers, k h ~ 140, where p = D d ~ e^(3 (th_r + th_s)) approaches the fp64 range;
+// such a determinant now goes to the GEPP re-evaluation like an overflowing one.)
 constexpr int kKeyMultMax = kBlockMultExp << 20;
-constexpr unsigned kKeyNormMin = 0x00100000u, kKeyRange = 0x7ff00000u - 0x00100000u;
+#ifndef MASW_KEY_PMAX
+#define MASW_KEY_PMAX 0x7fd00000u   // key(2^1022) (variant builds: 0x7ff00000u, the old bound)
+#endif
+constexpr unsigned kKeyNormMin = 0x00100000u, kKeyRange = MASW_KEY_PMAX - 0x00100000u;
 
 // State of one block-recursion sign evaluation (see det_sign_block).
 struct BlockSign {
@@ -1466,8 +1473,9 @@ struct BlockSign {
 // i.e. one reciprocal of p_t = D_t d_t per node and none per element; the last node
 // S_N = f_(N-1) X / d + K_hs is scaled by the real d / f_(N-1):  Z = X + p K_hs / (rho_(N-1) c^2)
 // (same sign of Re det).  The half-space is passed pre-scaled (halfspace_k with
-// mu' = rho_N beta_N^2 / (rho_(N-1) c^2)).  p_t is also certified (nonzero, finite: D_t = 0 is
-// a pole of the element, which the GEPP re-evaluation reports as non-finite).
+// mu' = rho_N beta_N^2 / (rho_(N-1) c^2)).  p_t is also certified (normal, with a normal
+// reciprocal: D_t = 0 is a pole of the element, which the GEPP re-evaluation reports as
+// non-finite).
 struct BlockSignU {
     ElemU P;                // the previous layer's element
     double s11, s12, s22;   // S^_t

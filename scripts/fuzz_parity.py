@@ -1,0 +1,104 @@
+"""Randomised parity sweep (evidence run, not a unit test): many seeded calls with random
+shapes -- N = 1..12 layers, random layered models (synth.random_models: reversals, stiff lids,
+soft channels), random wavelength ranges on both sides of the fine/coarse cosh/sinh table
+boundary (k h_max <= 50.5 or above), grids from 0.5 m/s or from near the slowest layer, every
+scan (model-major, pair, row) -- each compared with the CPU oracle row by row under the S16
+near-root rule (tests/masw_parity.py::ct_acceptable).  Writes one JSON summary.
+
+    python scripts/fuzz_parity.py [seconds] [out.json]
+"""
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import masw_parity as parity  # noqa: E402
+import oracle  # noqa: E402
+import paper_2003_02256_b200 as masw  # noqa: E402
+import synth  # noqa: E402
+
+
+KH_LO = float(os.environ.get("FUZZ_KH_LO", "50.6"))   # coarse calls: k h_max range
+KH_HI = float(os.environ.get("FUZZ_KH_HI", "300"))
+SEED = int(os.environ.get("FUZZ_SEED", "2003"))
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+    out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "fuzz_parity.json")
+    oracle.build()
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+    rng = np.random.Generator(np.random.PCG64(SEED))
+    t_end = time.time() + budget
+    stats = {"calls": 0, "rows": 0, "rows_equal": 0, "rows_one_step_S16": 0, "rows_bad": 0,
+             "fine_calls": 0, "coarse_calls": 0, "by_kernel": {}, "bad_cases": []}
+    call = 0
+    while time.time() < t_end:
+        call += 1
+        N = int(rng.integers(1, 13))
+        M = int(rng.integers(1, 60))
+        mods = synth.random_models(M, N, 10_000 + call)
+        hmax = float(mods.h.max())
+        fine = bool(rng.integers(0, 2))
+        khmax = float(rng.uniform(5.0, 50.4)) if fine else float(rng.uniform(KH_LO, KH_HI))
+        lam_min = 2 * math.pi * hmax / khmax
+        L = int(rng.integers(1, 48))
+        lam = synth.geom(float(rng.uniform(max(lam_min * 1.5, 2.0), 120.0)), lam_min, L) if L > 1 \
+            else np.array([lam_min])
+        V = int(rng.integers(64, 1500))
+        if rng.integers(0, 2):
+            c = 0.5 * (np.arange(V, dtype=np.float64) + 1.0)           # from 0.5 m/s
+        else:
+            c0 = float(mods.beta.min()) * float(rng.uniform(0.5, 0.95))
+            c = c0 + float(rng.uniform(0.05, 1.0)) * np.arange(V, dtype=np.float64)
+        kern = ["models", "pairs", "rows"][int(rng.integers(0, 3))]
+        flag = {"models": masw.SCHED_MODELS, "pairs": masw.SCHED_PAIRS, "rows": masw.SCHED_ROWS}[kern]
+        try:
+            r = masw.masw_curves_ensemble(*[dev(x) for x in (mods.h, mods.alpha, mods.beta,
+                                                                mods.rho)], dev(lam), dev(c),
+                                          flags=flag)
+        except masw.MaswError as e:   # (e.g. k h > 350 cannot occur here; report anyway)
+            stats["bad_cases"].append({"call": call, "error": e.code})
+            continue
+        gidx = r.idx.cpu().numpy()
+        o = oracle.ensemble(mods, lam, c, None)
+        stats["calls"] += 1
+        stats["fine_calls" if fine else "coarse_calls"] += 1
+        k = stats["by_kernel"].setdefault(kern, {"calls": 0, "rows": 0, "bad": 0})
+        k["calls"] += 1
+        k["rows"] += gidx.size
+        stats["rows"] += gidx.size
+        eq = gidx == o["idx"]
+        stats["rows_equal"] += int(eq.sum())
+        for m in range(M):
+            if eq[m].all():
+                continue
+            a = (mods.h[m], mods.alpha[m], mods.beta[m], mods.rho[m])
+            ok, exact, one = parity.ct_acceptable(oracle, a, lam, c, gidx[m], o["idx"][m])
+            nb = int((~ok).sum())
+            stats["rows_one_step_S16"] += int(one)
+            stats["rows_bad"] += nb
+            k["bad"] += nb
+            if nb:
+                bad_i = np.nonzero(~ok)[0]
+                stats["bad_cases"].append({"call": call, "model": m, "N": N, "kernel": kern,
+                                           "fine": fine, "rows_bad": nb,
+                                           "kh_model": [float(2 * math.pi / lam[i] * mods.h[m].max())
+                                                        for i in bad_i]})
+        kh_rows = 2 * math.pi / lam[None, :] * mods.h.max(axis=1)[:, None]
+        for lo in (50, 80, 100, 120, 140, 160):
+            key = f"rows_kh_ge_{lo}"
+            stats[key] = stats.get(key, 0) + int((kh_rows >= lo).sum())
+    json.dump(stats, open(out, "w"), indent=1)
+    print(json.dumps({k: v for k, v in stats.items() if k != "bad_cases"}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

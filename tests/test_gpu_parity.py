@@ -832,3 +832,50 @@ def test_random_models_parity_fine_table(masw, orc, N, seed):
         a = [dev(x[m]) for x in (mods.h, mods.alpha, mods.beta, mods.rho)]
         st_p, ct_p, idx_p = masw.masw_curve(*a, dev(lam), dev(c), flags=masw.SCHED_PAIRS)
         assert np.array_equal(idx_p.cpu().numpy(), idx_r[m])
+
+
+@pytest.mark.parametrize("calls", [(76, 201, 446, 500), (651, 1740, 1774)])
+def test_thick_layer_reciprocal_range(masw, orc, calls):
+    """Thick layers (k h ~ 140-175, from scripts/fuzz_parity.py's seeded sweep): the block
+    recursion's p = D d comes within a factor 4 of the fp64 range, where its reciprocal
+    (rcp.approx.ftz) is subnormal and flushed; the certificate now requires |p| < 2^1022, so
+    such determinants are re-evaluated by the GEPP.  Before, every scan returned a false early
+    change on these rows (e.g. idx 608 vs the oracle's and binary128's 628).  All three scans
+    against the oracle under S16, zero violations."""
+    rng = np.random.Generator(np.random.PCG64(2003))
+    want = set(calls)
+    for call in range(1, max(calls) + 1):
+        # the draws of scripts/fuzz_parity.py in its order (uniforms inside conditionals kept)
+        N = int(rng.integers(1, 13))
+        M = int(rng.integers(1, 60))
+        mods = synth.random_models(M, N, 10_000 + call) if call in want else None
+        fine = bool(rng.integers(0, 2))
+        khmax = float(rng.uniform(5.0, 50.4)) if fine else float(rng.uniform(50.6, 300.0))
+        L = int(rng.integers(1, 48))
+        hmax = float(mods.h.max()) if mods is not None else 1.0
+        lam_min = 2 * math.pi * hmax / khmax
+        if L > 1:
+            lam = synth.geom(float(rng.uniform(max(lam_min * 1.5, 2.0), 120.0)), lam_min, L)
+        else:
+            lam = np.array([lam_min])
+        V = int(rng.integers(64, 1500))
+        if rng.integers(0, 2):
+            c = 0.5 * (np.arange(V, dtype=np.float64) + 1.0)
+        else:
+            bmin = float(mods.beta.min()) if mods is not None else 100.0
+            c0 = bmin * float(rng.uniform(0.5, 0.95))
+            c = c0 + float(rng.uniform(0.05, 1.0)) * np.arange(V, dtype=np.float64)
+        rng.integers(0, 3)                                     # (the sweep's kernel choice)
+        if call not in want:
+            continue
+        o = orc.ensemble(mods, lam, c, None)
+        for fl in (masw.SCHED_MODELS, masw.SCHED_PAIRS, masw.SCHED_ROWS):
+            st, ct, idx, _ = _ens(masw, mods, lam, c, None, fl, device=True)
+            bad = 0
+            for m in range(M):
+                if np.array_equal(idx[m], o["idx"][m]):
+                    continue
+                ok, exact, one = parity.ct_acceptable(orc, margs(mods, m), lam, c, idx[m],
+                                                      o["idx"][m])
+                bad += int((~ok).sum())
+            assert bad == 0, (call, fl, bad)
