@@ -28,6 +28,13 @@ import synth  # noqa: E402
 KH_LO = float(os.environ.get("FUZZ_KH_LO", "50.6"))   # coarse calls: k h_max range
 KH_HI = float(os.environ.get("FUZZ_KH_HI", "300"))
 SEED = int(os.environ.get("FUZZ_SEED", "2003"))
+# FUZZ_MODE: "default" as above; "stable" -- every call with MASW_STABLE (k h_max up to 340);
+# "wide" -- N up to 24 and grids reaching 2.5 x the fastest P wave (both waves trigonometric,
+# complex half-space node); "misc" -- N up to 40, host or device buffers, a random C_e
+# (misfit against the oracle's misfit of the GPU's C_t), random MASW_PIVOTED (MASW_DIRECT, an
+# A/B switch that drops the small-c pre-pass, is excluded: its small-c signs are noise,
+# reading S15'')
+MODE = os.environ.get("FUZZ_MODE", "default")
 
 
 def main():
@@ -37,38 +44,59 @@ def main():
     dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")
     rng = np.random.Generator(np.random.PCG64(SEED))
     t_end = time.time() + budget
-    stats = {"calls": 0, "rows": 0, "rows_equal": 0, "rows_one_step_S16": 0, "rows_bad": 0,
+    stats = {"mode": MODE, "seed": SEED, "calls": 0, "rows": 0, "rows_equal": 0, "rows_one_step_S16": 0, "rows_bad": 0,
              "fine_calls": 0, "coarse_calls": 0, "by_kernel": {}, "bad_cases": []}
     call = 0
     while time.time() < t_end:
         call += 1
-        N = int(rng.integers(1, 13))
-        M = int(rng.integers(1, 60))
+        N = int(rng.integers(1, {"wide": 25, "misc": 41}.get(MODE, 13)))
+        M = int(rng.integers(1, 12 if N > 12 else 60))
         mods = synth.random_models(M, N, 10_000 + call)
         hmax = float(mods.h.max())
         fine = bool(rng.integers(0, 2))
         khmax = float(rng.uniform(5.0, 50.4)) if fine else float(rng.uniform(KH_LO, KH_HI))
+        if MODE == "stable" and not fine:
+            khmax = float(rng.uniform(50.6, 340.0))   # (the oracle validates k h <= 350)
         lam_min = 2 * math.pi * hmax / khmax
         L = int(rng.integers(1, 48))
         lam = synth.geom(float(rng.uniform(max(lam_min * 1.5, 2.0), 120.0)), lam_min, L) if L > 1 \
             else np.array([lam_min])
         V = int(rng.integers(64, 1500))
-        if rng.integers(0, 2):
+        if MODE == "wide" and rng.integers(0, 2):
+            c_hi = 2.5 * float(mods.alpha.max())
+            c0 = float(rng.uniform(0.3, 1.0)) * float(mods.beta.min())
+            c = c0 + (c_hi - c0) / V * np.arange(V, dtype=np.float64)
+        elif rng.integers(0, 2):
             c = 0.5 * (np.arange(V, dtype=np.float64) + 1.0)           # from 0.5 m/s
         else:
             c0 = float(mods.beta.min()) * float(rng.uniform(0.5, 0.95))
             c = c0 + float(rng.uniform(0.05, 1.0)) * np.arange(V, dtype=np.float64)
         kern = ["models", "pairs", "rows"][int(rng.integers(0, 3))]
         flag = {"models": masw.SCHED_MODELS, "pairs": masw.SCHED_PAIRS, "rows": masw.SCHED_ROWS}[kern]
+        if MODE == "stable":
+            flag |= masw.STABLE
+        ce = None
+        host = False
+        if MODE == "misc":
+            flag |= [0, masw.PIVOTED][int(rng.integers(0, 2))]
+            host = bool(rng.integers(0, 2))
+            ce = float(mods.beta.min()) * rng.uniform(0.6, 1.1, len(lam))
+        conv = (lambda a: np.ascontiguousarray(a)) if host else dev
         try:
-            r = masw.masw_curves_ensemble(*[dev(x) for x in (mods.h, mods.alpha, mods.beta,
-                                                                mods.rho)], dev(lam), dev(c),
-                                          flags=flag)
+            r = masw.masw_curves_ensemble(*[conv(x) for x in (mods.h, mods.alpha, mods.beta,
+                                                                 mods.rho)], conv(lam), conv(c),
+                                          conv(ce) if ce is not None else None, flags=flag)
         except masw.MaswError as e:   # (e.g. k h > 350 cannot occur here; report anyway)
             stats["bad_cases"].append({"call": call, "error": e.code})
             continue
-        gidx = r.idx.cpu().numpy()
+        gidx = r.idx if host else r.idx.cpu().numpy()
         o = oracle.ensemble(mods, lam, c, None)
+        if ce is not None:   # misfit of the GPU's own C_t (reading S13), 1e-9 relative
+            gct = r.ct if host else r.ct.cpu().numpy()
+            gmis = r.misfit if host else r.misfit.cpu().numpy()
+            for m in range(M):
+                if not parity.misfit_ok(oracle, gct[m], ce, float(gmis[m])):
+                    stats["misfit_bad"] = stats.get("misfit_bad", 0) + 1
         stats["calls"] += 1
         stats["fine_calls" if fine else "coarse_calls"] += 1
         k = stats["by_kernel"].setdefault(kern, {"calls": 0, "rows": 0, "bad": 0})
@@ -89,7 +117,8 @@ def main():
             if nb:
                 bad_i = np.nonzero(~ok)[0]
                 stats["bad_cases"].append({"call": call, "model": m, "N": N, "kernel": kern,
-                                           "fine": fine, "rows_bad": nb,
+                                           "fine": fine, "rows_bad": nb, "flags": int(flag),
+                                           "host": host,
                                            "kh_model": [float(2 * math.pi / lam[i] * mods.h[m].max())
                                                         for i in bad_i]})
         kh_rows = 2 * math.pi / lam[None, :] * mods.h.max(axis=1)[:, None]
