@@ -34,6 +34,8 @@ SEED = int(os.environ.get("FUZZ_SEED", "2003"))
 # (misfit against the oracle's misfit of the GPU's C_t), random MASW_PIVOTED (MASW_DIRECT, an
 # A/B switch that drops the small-c pre-pass, is excluded: its small-c signs are noise,
 # reading S15'')
+# "s4" -- grids containing the models' own layer velocities and points within 1e-4 of them
+# (the perturbation rule, reading S4), 1-5 models per call
 MODE = os.environ.get("FUZZ_MODE", "default")
 
 
@@ -51,6 +53,8 @@ def main():
         call += 1
         N = int(rng.integers(1, {"wide": 25, "misc": 41}.get(MODE, 13)))
         M = int(rng.integers(1, 12 if N > 12 else 60))
+        if MODE == "s4":
+            M = int(rng.integers(1, 6))
         mods = synth.random_models(M, N, 10_000 + call)
         hmax = float(mods.h.max())
         fine = bool(rng.integers(0, 2))
@@ -71,6 +75,11 @@ def main():
         else:
             c0 = float(mods.beta.min()) * float(rng.uniform(0.5, 0.95))
             c = c0 + float(rng.uniform(0.05, 1.0)) * np.arange(V, dtype=np.float64)
+        if MODE == "s4":   # the models' velocities, and points just inside / outside 1e-4 of them
+            vel = np.concatenate([mods.alpha.ravel(), mods.beta.ravel()])
+            off = rng.choice(np.array([0.0, 0.0, 5e-5, -5e-5, 9.9e-5, -1.5e-4, 2e-4]), vel.size)
+            c = np.unique(np.concatenate([c, vel + off]))
+            c = c[c > 0]
         kern = ["models", "pairs", "rows"][int(rng.integers(0, 3))]
         flag = {"models": masw.SCHED_MODELS, "pairs": masw.SCHED_PAIRS, "rows": masw.SCHED_ROWS}[kern]
         if MODE == "stable":
