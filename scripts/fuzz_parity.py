@@ -42,6 +42,13 @@ MODE = os.environ.get("FUZZ_MODE", "default")
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     out = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "fuzz_parity.json")
+    stats = run(budget)
+    json.dump(stats, open(out, "w"), indent=1)
+    print(json.dumps({k: v for k, v in stats.items() if k != "bad_cases"}), flush=True)
+
+
+def run(budget: float, max_calls: int = 1 << 62) -> dict:
+    """The sweep for `budget` seconds or `max_calls` calls (whichever ends first)."""
     oracle.build()
     dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")
     rng = np.random.Generator(np.random.PCG64(SEED))
@@ -49,7 +56,7 @@ def main():
     stats = {"mode": MODE, "seed": SEED, "calls": 0, "rows": 0, "rows_equal": 0, "rows_one_step_S16": 0, "rows_bad": 0,
              "fine_calls": 0, "coarse_calls": 0, "by_kernel": {}, "bad_cases": []}
     call = 0
-    while time.time() < t_end:
+    while time.time() < t_end and call < max_calls:
         call += 1
         N = int(rng.integers(1, {"wide": 25, "misc": 41}.get(MODE, 13)))
         M = int(rng.integers(1, 12 if N > 12 else 60))
@@ -134,8 +141,7 @@ def main():
         for lo in (50, 80, 100, 120, 140, 160):
             key = f"rows_kh_ge_{lo}"
             stats[key] = stats.get(key, 0) + int((kh_rows >= lo).sum())
-    json.dump(stats, open(out, "w"), indent=1)
-    print(json.dumps({k: v for k, v in stats.items() if k != "bad_cases"}), flush=True)
+    return stats
 
 
 if __name__ == "__main__":
