@@ -1334,9 +1334,10 @@ __device__ __forceinline__ DetOut det_core(int Nrt, ElemFn &&elem, HsFn &&hs)
 // gives the sign with no pivot search, no branches and no row bookkeeping (~25 FP64 ops
 // per node, like one banded-GEPP step, but ~45 fewer integer / move / branch instructions).
 // Unpivoted elimination is backward stable when its multipliers W_t = S_t^{-1} B_t stay
-// bounded (threshold pivoting: then |L||U| <= (1 + |W|) |K| block-wise), so the sign is as
-// reliable as GEPP's; every step checks max|W_t| <= 2^kBlockMultExp (exponent arithmetic on
-// the high words) and that every det S_t is nonzero and finite.  A determinant that fails
+// bounded (threshold pivoting: then |L||U| <= (1 + |W|) |K| block-wise; the bound and the
+// measured agreement with GEPP are in DESIGN.md §5); every step checks max|W_t| <=
+// 2^kBlockMultExp (exponent arithmetic on the high words) and that every det S_t is nonzero
+// and finite (BlockSignU: every scaling p_t normal with a normal reciprocal).  A determinant that fails
 // the check (a leading block S_t nearly singular: rare, measured in DESIGN.md) is re-evaluated
 // by the caller with the banded GEPP (det_core), so the result always follows partial
 // pivoting where the unpivoted recursion is not certified.  (Reading S11: the values of
