@@ -4,7 +4,7 @@ stable element) against the oracle's dense complex LU on random layered models a
 |det| >= 1e-12 of the row maximum, kappa <= 1e-10), and the sign of Re det wherever the det
 is in that domain.  Writes one JSON summary.
 
-    python scripts/fuzz_detgrid.py [seconds] [out.json]
+    python tests/fuzz/fuzz_detgrid.py [seconds] [out.json]
 """
 import json
 import math
@@ -12,7 +12,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402

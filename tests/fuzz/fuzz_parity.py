@@ -5,7 +5,7 @@ boundary (k h_max <= 50.5 or above), grids from 0.5 m/s or from near the slowest
 scan (model-major, pair, row) -- each compared with the CPU oracle row by row under the S16
 near-root rule (tests/masw_parity.py::ct_acceptable).  Writes one JSON summary.
 
-    python scripts/fuzz_parity.py [seconds] [out.json]
+    python tests/fuzz/fuzz_parity.py [seconds] [out.json]
 """
 import json
 import math
@@ -13,7 +13,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402

@@ -1,16 +1,16 @@
-"""Replays scripts/fuzz_parity.py's seeded call sequence and, for the calls listed in its
+"""Replays tests/fuzz/fuzz_parity.py's seeded call sequence and, for the calls listed in its
 JSON summary's bad_cases, prints per disagreeing row: the GPU and oracle indices, and around
 both the sign of Re det K from the oracle in fp64 and in binary128 (det_quad) -- which side
 is right (development aid).
 
-    python scripts/fuzz_replay.py gpurun_out/fuzz_parity.json [max_cases]
+    python tests/fuzz/fuzz_replay.py gpurun_out/fuzz_parity.json [max_cases]
 """
 import json
 import math
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402

@@ -1,4 +1,4 @@
-"""A bounded run of the randomised parity sweep (scripts/fuzz_parity.py, seed 2003, the first
+"""A bounded run of the randomised parity sweep (tests/fuzz/fuzz_parity.py, seed 2003, the first
 450 calls: random layered models N = 1..12, wavelength ranges on both sides of the fine/coarse
 cosh/sinh table boundary up to k h = 300, grids from 0.5 m/s or near the slowest layer, every
 scan), each call's C_t against the CPU oracle under the S16 rule.  The full sweeps and their
@@ -18,7 +18,7 @@ def test_random_sweep_first_450_calls():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    sys.path.insert(0, os.path.join(ROOT, "tests", "fuzz"))
     os.environ.setdefault("FUZZ_SEED", "2003")
     import fuzz_parity
 

@@ -836,7 +836,7 @@ def test_random_models_parity_fine_table(masw, orc, N, seed):
 
 @pytest.mark.parametrize("calls", [(76, 201, 446, 500), (651, 1740, 1774)])
 def test_thick_layer_reciprocal_range(masw, orc, calls):
-    """Thick layers (k h ~ 140-175, from scripts/fuzz_parity.py's seeded sweep): the block
+    """Thick layers (k h ~ 140-175, from tests/fuzz/fuzz_parity.py's seeded sweep): the block
     recursion's p = D d comes within a factor 4 of the fp64 range, where its reciprocal
     (rcp.approx.ftz) is subnormal and flushed; the certificate now requires |p| < 2^1022, so
     such determinants are re-evaluated by the GEPP.  Before, every scan returned a false early
@@ -845,7 +845,7 @@ def test_thick_layer_reciprocal_range(masw, orc, calls):
     rng = np.random.Generator(np.random.PCG64(2003))
     want = set(calls)
     for call in range(1, max(calls) + 1):
-        # the draws of scripts/fuzz_parity.py in its order (uniforms inside conditionals kept)
+        # the draws of tests/fuzz/fuzz_parity.py in its order (uniforms inside conditionals kept)
         N = int(rng.integers(1, 13))
         M = int(rng.integers(1, 60))
         mods = synth.random_models(M, N, 10_000 + call) if call in want else None
