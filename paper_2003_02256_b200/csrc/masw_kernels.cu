@@ -1639,7 +1639,7 @@ __device__ __forceinline__ void scan_pair_body(ScanArgs a)
             }
             for (int q = 0; q < 2; ++q) {
                 const bool p = q ? pend1 : pend0;
-                if (!p) return;
+                if (!p) continue;   // (the q loop: the other row may still need its write)
                 team_alg += (unsigned long long)V;
                 if (lane == 0) {
                     const long long r = r0 + q;

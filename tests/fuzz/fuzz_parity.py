@@ -34,9 +34,62 @@ SEED = int(os.environ.get("FUZZ_SEED", "2003"))
 # (misfit against the oracle's misfit of the GPU's C_t), random MASW_PIVOTED (MASW_DIRECT, an
 # A/B switch that drops the small-c pre-pass, is excluded: its small-c signs are noise,
 # reading S15'')
+# "big" -- 3000-8000 models per call, N = 3..8, the automatic kernel choice (model-major scan
+# with its tail pieces, or the pair scan), no forced schedule
 # "s4" -- grids containing the models' own layer velocities and points within 1e-4 of them
 # (the perturbation rule, reading S4), 1-5 models per call
 MODE = os.environ.get("FUZZ_MODE", "default")
+
+
+def make_call(rng, call):
+    """One call of the sweep (the seeded draws in their fixed order): the models, wavelengths,
+    grid, kernel label, flags, C_e (or None) and whether host buffers are used."""
+    N = int(rng.integers(1, {"wide": 25, "misc": 41}.get(MODE, 13)))
+    M = int(rng.integers(1, 12 if N > 12 else 60))
+    if MODE == "s4":
+        M = int(rng.integers(1, 6))
+    if MODE == "big":
+        N = int(rng.integers(3, 9))
+        M = int(rng.integers(3000, 8001))
+    mods = synth.random_models(M, N, 10_000 + call)
+    hmax = float(mods.h.max())
+    fine = bool(rng.integers(0, 2))
+    khmax = float(rng.uniform(5.0, 50.4)) if fine else float(rng.uniform(KH_LO, KH_HI))
+    if MODE == "stable" and not fine:
+        khmax = float(rng.uniform(50.6, 340.0))   # (the oracle validates k h <= 350)
+    lam_min = 2 * math.pi * hmax / khmax
+    L = int(rng.integers(1, 48))
+    lam = synth.geom(float(rng.uniform(max(lam_min * 1.5, 2.0), 120.0)), lam_min, L) if L > 1 \
+        else np.array([lam_min])
+    V = int(rng.integers(64, 1500))
+    if MODE == "wide" and rng.integers(0, 2):
+        c_hi = 2.5 * float(mods.alpha.max())
+        c0 = float(rng.uniform(0.3, 1.0)) * float(mods.beta.min())
+        c = c0 + (c_hi - c0) / V * np.arange(V, dtype=np.float64)
+    elif rng.integers(0, 2):
+        c = 0.5 * (np.arange(V, dtype=np.float64) + 1.0)           # from 0.5 m/s
+    else:
+        c0 = float(mods.beta.min()) * float(rng.uniform(0.5, 0.95))
+        c = c0 + float(rng.uniform(0.05, 1.0)) * np.arange(V, dtype=np.float64)
+    if MODE == "s4":   # the models' velocities, and points just inside / outside 1e-4 of them
+        vel = np.concatenate([mods.alpha.ravel(), mods.beta.ravel()])
+        off = rng.choice(np.array([0.0, 0.0, 5e-5, -5e-5, 9.9e-5, -1.5e-4, 2e-4]), vel.size)
+        c = np.unique(np.concatenate([c, vel + off]))
+        c = c[c > 0]
+    kern = ["models", "pairs", "rows"][int(rng.integers(0, 3))]
+    flag = {"models": masw.SCHED_MODELS, "pairs": masw.SCHED_PAIRS, "rows": masw.SCHED_ROWS}[kern]
+    if MODE == "stable":
+        flag |= masw.STABLE
+    if MODE == "big":
+        flag = 0
+        kern = "auto"
+    ce = None
+    host = False
+    if MODE == "misc":
+        flag |= [0, masw.PIVOTED][int(rng.integers(0, 2))]
+        host = bool(rng.integers(0, 2))
+        ce = float(mods.beta.min()) * rng.uniform(0.6, 1.1, len(lam))
+    return N, M, mods, fine, khmax, lam, c, kern, flag, ce, host
 
 
 def main():
@@ -58,45 +111,7 @@ def run(budget: float, max_calls: int = 1 << 62) -> dict:
     call = 0
     while time.time() < t_end and call < max_calls:
         call += 1
-        N = int(rng.integers(1, {"wide": 25, "misc": 41}.get(MODE, 13)))
-        M = int(rng.integers(1, 12 if N > 12 else 60))
-        if MODE == "s4":
-            M = int(rng.integers(1, 6))
-        mods = synth.random_models(M, N, 10_000 + call)
-        hmax = float(mods.h.max())
-        fine = bool(rng.integers(0, 2))
-        khmax = float(rng.uniform(5.0, 50.4)) if fine else float(rng.uniform(KH_LO, KH_HI))
-        if MODE == "stable" and not fine:
-            khmax = float(rng.uniform(50.6, 340.0))   # (the oracle validates k h <= 350)
-        lam_min = 2 * math.pi * hmax / khmax
-        L = int(rng.integers(1, 48))
-        lam = synth.geom(float(rng.uniform(max(lam_min * 1.5, 2.0), 120.0)), lam_min, L) if L > 1 \
-            else np.array([lam_min])
-        V = int(rng.integers(64, 1500))
-        if MODE == "wide" and rng.integers(0, 2):
-            c_hi = 2.5 * float(mods.alpha.max())
-            c0 = float(rng.uniform(0.3, 1.0)) * float(mods.beta.min())
-            c = c0 + (c_hi - c0) / V * np.arange(V, dtype=np.float64)
-        elif rng.integers(0, 2):
-            c = 0.5 * (np.arange(V, dtype=np.float64) + 1.0)           # from 0.5 m/s
-        else:
-            c0 = float(mods.beta.min()) * float(rng.uniform(0.5, 0.95))
-            c = c0 + float(rng.uniform(0.05, 1.0)) * np.arange(V, dtype=np.float64)
-        if MODE == "s4":   # the models' velocities, and points just inside / outside 1e-4 of them
-            vel = np.concatenate([mods.alpha.ravel(), mods.beta.ravel()])
-            off = rng.choice(np.array([0.0, 0.0, 5e-5, -5e-5, 9.9e-5, -1.5e-4, 2e-4]), vel.size)
-            c = np.unique(np.concatenate([c, vel + off]))
-            c = c[c > 0]
-        kern = ["models", "pairs", "rows"][int(rng.integers(0, 3))]
-        flag = {"models": masw.SCHED_MODELS, "pairs": masw.SCHED_PAIRS, "rows": masw.SCHED_ROWS}[kern]
-        if MODE == "stable":
-            flag |= masw.STABLE
-        ce = None
-        host = False
-        if MODE == "misc":
-            flag |= [0, masw.PIVOTED][int(rng.integers(0, 2))]
-            host = bool(rng.integers(0, 2))
-            ce = float(mods.beta.min()) * rng.uniform(0.6, 1.1, len(lam))
+        N, M, mods, fine, khmax, lam, c, kern, flag, ce, host = make_call(rng, call)
         conv = (lambda a: np.ascontiguousarray(a)) if host else dev
         try:
             r = masw.masw_curves_ensemble(*[conv(x) for x in (mods.h, mods.alpha, mods.beta,

@@ -879,3 +879,27 @@ def test_thick_layer_reciprocal_range(masw, orc, calls):
                                                       o["idx"][m])
                 bad += int((~ok).sum())
             assert bad == 0, (call, fl, bad)
+
+
+def test_pair_scan_whole_pairs_with_unfinished_partner(masw, orc):
+    """Whole-pair items of the pair scan (more pairs than resident warps, so not tail
+    segments) where one row of a pair changes sign on the grid and the other does not: both
+    rows' outputs must be written (a round-2 regression wrote only the first: the second row
+    kept idx 0, found by tests/fuzz/fuzz_parity.py's "big" mode).  One model (C4's), 6000
+    wavelengths in random order (reading S17), a grid ending below the long wavelengths'
+    phase velocities: the pair scan equals the row scan bitwise and the oracle on a sample."""
+    w = synth.workload("realistic")
+    m = w.models
+    rng = np.random.Generator(np.random.PCG64(17))
+    lam = rng.permutation(w.lam)[:6000]
+    c = 15.0 + 0.05 * np.arange(2000, dtype=np.float64)          # to 115 m/s
+    a = [dev(x[0]) for x in (m.h, m.alpha, m.beta, m.rho)]
+    st_p, ct_p, idx_p = masw.masw_curve(*a, dev(lam), dev(c), flags=masw.SCHED_PAIRS)
+    st_r, ct_r, idx_r = masw.masw_curve(*a, dev(lam), dev(c), flags=masw.SCHED_ROWS)
+    ip, ir = idx_p.cpu().numpy(), idx_r.cpu().numpy()
+    assert (ir == -1).sum() > 500 and (ir > 0).sum() > 500      # both kinds of rows
+    assert st_p == st_r and np.array_equal(ip, ir)
+    assert np.array_equal(ct_p.cpu().numpy(), ct_r.cpu().numpy(), equal_nan=True)
+    sel = np.arange(0, 6000, 60)
+    ost, oct_, oidx, _ = orc.curve(*margs(m), lam[sel], c)
+    assert np.array_equal(ip[sel], oidx)
