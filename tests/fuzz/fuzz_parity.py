@@ -39,6 +39,7 @@ SEED = int(os.environ.get("FUZZ_SEED", "2003"))
 # "s4" -- grids containing the models' own layer velocities and points within 1e-4 of them
 # (the perturbation rule, reading S4), 1-5 models per call
 MODE = os.environ.get("FUZZ_MODE", "default")
+EXTRA_FLAGS = int(os.environ.get("FUZZ_FLAGS", "0"), 0)   # OR-ed into every call's flags
 
 
 def make_call(rng, call):
@@ -83,6 +84,7 @@ def make_call(rng, call):
     if MODE == "big":
         flag = 0
         kern = "auto"
+    flag |= EXTRA_FLAGS
     ce = None
     host = False
     if MODE == "misc":
@@ -106,7 +108,7 @@ def run(budget: float, max_calls: int = 1 << 62) -> dict:
     dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device="cuda")
     rng = np.random.Generator(np.random.PCG64(SEED))
     t_end = time.time() + budget
-    stats = {"mode": MODE, "seed": SEED, "calls": 0, "rows": 0, "rows_equal": 0, "rows_one_step_S16": 0, "rows_bad": 0,
+    stats = {"mode": MODE, "seed": SEED, "extra_flags": EXTRA_FLAGS, "calls": 0, "rows": 0, "rows_equal": 0, "rows_one_step_S16": 0, "rows_bad": 0,
              "fine_calls": 0, "coarse_calls": 0, "by_kernel": {}, "bad_cases": []}
     call = 0
     while time.time() < t_end and call < max_calls:
