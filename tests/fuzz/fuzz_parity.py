@@ -36,6 +36,8 @@ SEED = int(os.environ.get("FUZZ_SEED", "2003"))
 # reading S15'')
 # "big" -- 3000-8000 models per call, N = 3..8, the automatic kernel choice (model-major scan
 # with its tail pieces, or the pair scan), no forced schedule
+# "curve" -- one model, 3000-12000 wavelengths in random order (single long curves: whole
+# pairs plus tail segments of the pair scan), the automatic kernel choice
 # "s4" -- grids containing the models' own layer velocities and points within 1e-4 of them
 # (the perturbation rule, reading S4), 1-5 models per call
 MODE = os.environ.get("FUZZ_MODE", "default")
@@ -52,6 +54,8 @@ def make_call(rng, call):
     if MODE == "big":
         N = int(rng.integers(3, 9))
         M = int(rng.integers(3000, 8001))
+    if MODE == "curve":
+        M = 1
     mods = synth.random_models(M, N, 10_000 + call)
     hmax = float(mods.h.max())
     fine = bool(rng.integers(0, 2))
@@ -60,8 +64,12 @@ def make_call(rng, call):
         khmax = float(rng.uniform(50.6, 340.0))   # (the oracle validates k h <= 350)
     lam_min = 2 * math.pi * hmax / khmax
     L = int(rng.integers(1, 48))
+    if MODE == "curve":
+        L = int(rng.integers(3000, 12001))
     lam = synth.geom(float(rng.uniform(max(lam_min * 1.5, 2.0), 120.0)), lam_min, L) if L > 1 \
         else np.array([lam_min])
+    if MODE == "curve":
+        lam = rng.permutation(lam)
     V = int(rng.integers(64, 1500))
     if MODE == "wide" and rng.integers(0, 2):
         c_hi = 2.5 * float(mods.alpha.max())
@@ -81,7 +89,7 @@ def make_call(rng, call):
     flag = {"models": masw.SCHED_MODELS, "pairs": masw.SCHED_PAIRS, "rows": masw.SCHED_ROWS}[kern]
     if MODE == "stable":
         flag |= masw.STABLE
-    if MODE == "big":
+    if MODE in ("big", "curve"):
         flag = 0
         kern = "auto"
     flag |= EXTRA_FLAGS
