@@ -93,7 +93,8 @@ typedef struct {
 
 /* exec.flags */
 #define MASW_ASYNC 0x1u       /* device pointers: no status readback, return after enqueue  */
-#define MASW_TIME_SCAN 0x2u   /* record CUDA events around the scan (small-c prefix + scan kernel; masw_last_scan_ms) */
+#define MASW_TIME_SCAN 0x2u   /* record CUDA events around the scan kernels (both cosh/sinh table
+                                 instances; not the small-c pre-pass): masw_last_scan_ms */
 /* Row schedule of the scan (default: a work-stealing queue over rows, lambda-major).  The two
  * static schedules are the paper's partitions, here over the kernel's teams:
  * team g of G takes a contiguous block of rows, or rows g, g+G, g+2G, ... (load-balance

@@ -309,7 +309,6 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
                 CK(cudaEventCreate(&slot[1]));
                 sdev = dev + 1;
             }
-            CK(cudaEventRecord(slot[0], st));
         }
         // reading S15'': the rows' small-c prefixes with the stable element, before the scan
         if (!stable && !(ex.flags & MASW_DIRECT)) {
@@ -323,6 +322,7 @@ int run_curves(const ModelArgs &mod_in, const double *lam, int64_t L, const doub
             sa.pstart = pst;
             sa.pcarry = pca;
         }
+        if (timed) CK(cudaEventRecord(slot[0], st));   // the scan kernels only
         if (models) {
             CK(launch_scan_models(sa, st, dev));
         } else if (pairs) {
